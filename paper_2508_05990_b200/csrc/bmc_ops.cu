@@ -1,0 +1,416 @@
+// Ingest, MV refinement, AEM frame selection and motion compensation kernels
+// (sm_100a).  All integer work is bit-exact by construction; the float64 work
+// (energy re-evaluation, AEM accumulation and statistics) follows the
+// reference's operation order with explicitly rounded intrinsics.
+#include <cstdio>
+
+#include "bmc_internal.cuh"
+#include "bmc_launch.cuh"
+
+namespace bmc {
+
+// ---------------------------------------------------------------------------
+// Ingest: raw (frames, H, W) -> padded packed planes (frame_io.py:173-184,
+// fme.py:181-211).  One thread writes one 32-bit word of one plane row; padded
+// rows/columns replicate the last real sample (np.pad mode="edge").  Columns in
+// [pad_w, pitch) are filled the same way so staging may read whole words.
+// ---------------------------------------------------------------------------
+template <typename Elem>
+__global__ void pack_kernel(const Elem* __restrict__ raw, long long n_words, int kind, int H, int W,
+                            const bmc_fme_params p, Elem* __restrict__ planes) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  const int wpr = p.pitch / EPW;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n_words;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long t = idx;
+    const int w = (int)(t % wpr);
+    t /= wpr;
+    const int y = (int)(t % p.pad_h);
+    t /= p.pad_h;
+    const int pl = (int)(t % p.planes);
+    const long long f = t / p.planes;
+    const int ys = min(y, p.real_h - 1);
+    const Elem* src;
+    int step, x0;
+    if (kind == BMC_KIND_BAYER) {
+      src = raw + f * H * (long long)W + (long long)(2 * ys + (pl >> 1)) * W;
+      step = 2;
+      x0 = pl & 1;
+    } else {
+      src = raw + f * H * (long long)W + (long long)ys * W;
+      step = 1;
+      x0 = 0;
+    }
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < EPW; ++e) {
+      const int xs = min(w * EPW + e, p.real_w - 1);
+      word |= (uint32_t)__ldg(src + x0 + step * xs) << (8 * sizeof(Elem) * e);
+    }
+    reinterpret_cast<uint32_t*>(planes + f * p.frame_stride + pl * p.plane_stride + (long long)y * p.pitch)[w] = word;
+  }
+}
+
+int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p, void* planes, cudaStream_t st) {
+  const int epw = 4 / p.elem_bytes;
+  const long long n_words = (long long)n_frames * p.planes * p.pad_h * (p.pitch / epw);
+  const int blocks = (int)((n_words + kThreads - 1) / kThreads < 148 * 16 ? (n_words + kThreads - 1) / kThreads
+                                                                          : 148 * 16);
+  const int H = p.planes == 4 ? p.real_h * 2 : p.real_h;
+  const int W = p.planes == 4 ? p.real_w * 2 : p.real_w;
+  if (p.elem_bytes == 1)
+    pack_kernel<uint8_t><<<blocks, kThreads, 0, st>>>((const uint8_t*)raw, n_words, kind, H, W, p, (uint8_t*)planes);
+  else
+    pack_kernel<uint16_t><<<blocks, kThreads, 0, st>>>((const uint16_t*)raw, n_words, kind, H, W, p,
+                                                       (uint16_t*)planes);
+  return cuda_status(cudaGetLastError(), "pack_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// fl(v / 65535) table for the uint16 exact replay.
+// ---------------------------------------------------------------------------
+__global__ void norm_table_kernel(double* tab, int n, double s) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) tab[v] = __ddiv_rn((double)v, s);
+}
+
+const double* norm_table_u16(int device) {
+  static double* tabs[64] = {nullptr};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!tabs[device]) {
+    double* t = nullptr;
+    if (cudaMalloc(&t, 65536 * sizeof(double)) != cudaSuccess) return nullptr;
+    norm_table_kernel<<<256, 256>>>(t, 65536, 65535.0);
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    tabs[device] = t;
+  }
+  return tabs[device];
+}
+
+// ---------------------------------------------------------------------------
+// MV refinement (mv_refine.py:17-69).  One warp per block: lane 0 takes the
+// clipped 3x3 window of the INPUT field, the lower-middle order statistic of
+// each component, and the Chebyshev test; replaced blocks re-evaluate their
+// energy with the warp-cooperative exact replay on the padded planes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int lower_median(int* v, int n) {
+  for (int i = 1; i < n; ++i) {  // insertion sort (<= 9 entries)
+    const int x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) {
+      v[j + 1] = v[j];
+      --j;
+    }
+    v[j + 1] = x;
+  }
+  return v[(n - 1) / 2];
+}
+
+template <typename Elem>
+__global__ void __launch_bounds__(kThreads) refine_kernel(const RefineArgs a) {
+  __shared__ double tab8[256];
+  const bmc_fme_params& p = a.prm;
+  const double* tab = a.tab16;
+  if (sizeof(Elem) == 1) {
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) tab8[v] = __ddiv_rn((double)v, (double)p.max_value);
+    tab = tab8;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long cells = (long long)a.n_pairs * a.gh * a.gw;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (wid >= cells) return;
+  const int pair = (int)(wid / ((long long)a.gh * a.gw));
+  const int cell = (int)(wid % ((long long)a.gh * a.gw));
+  const int gy = cell / a.gw, gx = cell % a.gw;
+  const int32_t* mv = a.mv_in + (long long)pair * a.gh * a.gw * 2;
+  int mx = 0, my = 0, rep = 0;
+  if (lane == 0) {
+    int vx[9], vy[9], n = 0;
+    for (int y = max(0, gy - 1); y < min(a.gh, gy + 2); ++y)
+      for (int x = max(0, gx - 1); x < min(a.gw, gx + 2); ++x) {
+        vx[n] = mv[2 * (y * a.gw + x)];
+        vy[n] = mv[2 * (y * a.gw + x) + 1];
+        ++n;
+      }
+    const int medx = lower_median(vx, n), medy = lower_median(vy, n);
+    mx = mv[2 * cell];
+    my = mv[2 * cell + 1];
+    const int dev = max(abs(mx - medx), abs(my - medy));
+    if (dev > a.thr) {
+      mx = medx;
+      my = medy;
+      rep = 1;
+    }
+  }
+  mx = __shfl_sync(0xffffffffu, mx, 0);
+  my = __shfl_sync(0xffffffffu, my, 0);
+  rep = __shfl_sync(0xffffffffu, rep, 0);
+  const long long o = (long long)pair * a.gh * a.gw + cell;
+  double e = a.e_in[o];
+  if (rep && a.planes) {
+    const int ox = gx * a.b, oy = gy * a.b;
+    const int rx = ox + mx, ry = oy + my;
+    if (rx >= 0 && rx <= p.pad_w - a.b && ry >= 0 && ry <= p.pad_h - a.b) {  // mv_refine.py:60
+      const Elem* base = reinterpret_cast<const Elem*>(a.planes);
+      const Elem* cur = base + (long long)a.cur_index[pair] * p.frame_stride + (long long)oy * p.pitch + ox;
+      const Elem* ref = base + (long long)a.ref_index[pair] * p.frame_stride + (long long)ry * p.pitch + rx;
+      e = exact_energy_warp<Elem>(cur, ref, p.pitch, p.plane_stride, a.b, p.planes, tab, p.sparsity_tolerance,
+                                  p.one_minus_lam, p.lam)
+              .energy;
+    }
+  }
+  if (lane == 0) {
+    a.mv_out[2 * o] = mx;
+    a.mv_out[2 * o + 1] = my;
+    a.e_out[o] = e;
+    if (a.replaced) a.replaced[o] = rep;
+  }
+}
+
+int launch_refine(const RefineArgs& a, cudaStream_t st) {
+  const long long warps = (long long)a.n_pairs * a.gh * a.gw;
+  const long long blocks = (warps * 32 + kThreads - 1) / kThreads;
+  if (a.prm.elem_bytes == 1)
+    refine_kernel<uint8_t><<<(unsigned)blocks, kThreads, 0, st>>>(a);
+  else
+    refine_kernel<uint16_t><<<(unsigned)blocks, kThreads, 0, st>>>(a);
+  return cuda_status(cudaGetLastError(), "refine_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// AEM frame selection (frame_select.py:74-136).  One CTA per stream scans its
+// frames in order: pooled = max over factor x factor children
+// (frame_select.py:96), acc += pooled, trigger = max (exact) or numpy pairwise
+// mean, key iff trigger > thr or frames_since_key+1 >= max_gop.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) decide_kernel(const DecideArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[kWarps];
+  __shared__ double result;
+  const int stream = blockIdx.x;
+  const bmc_select_params& sp = a.sp;
+  const int ncoarse = sp.coarse_h * sp.coarse_w;
+  double* acc = a.acc + (long long)stream * ncoarse;
+  const long long nleaf = a.nleaf;
+  long long* leaf_lo = reinterpret_cast<long long*>(smem_raw);
+  double* leaf_val = reinterpret_cast<double*>(leaf_lo + nleaf);
+  int* leaf_len = reinterpret_cast<int*>(leaf_val + nleaf) + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = a.t_begin; t < a.t_end; ++t) {
+    const double* e = a.energy + stream * a.ess + t * a.efs;
+    double mx = -INFINITY;
+    for (int c = threadIdx.x; c < ncoarse; c += blockDim.x) {
+      const int cy = c / sp.coarse_w, cx = c % sp.coarse_w;
+      double pooled;
+      if (sp.factor == 1) {
+        pooled = e[c];
+      } else {
+        pooled = -INFINITY;
+        for (int dy = 0; dy < sp.factor; ++dy)
+          for (int dx = 0; dx < sp.factor; ++dx)
+            pooled = fmax(pooled, e[(cy * sp.factor + dy) * sp.grid_w + cx * sp.factor + dx]);
+      }
+      const double v = __dadd_rn(acc[c], pooled);
+      acc[c] = v;
+      mx = fmax(mx, v);
+    }
+    double trig;
+    if (!sp.statistic_mean) {
+      for (int m = 16; m; m >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+      if (lane == 0) red[warp] = mx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double r = red[0];
+        for (int w = 1; w < kWarps; ++w) r = fmax(r, red[w]);
+        result = r;
+      }
+      __syncthreads();
+      trig = result;
+    } else {
+      const double s = block_pairwise([&](long long i) { return acc[i]; }, ncoarse, leaf_lo, leaf_len, leaf_val,
+                                      &result);
+      trig = __ddiv_rn(s, (double)ncoarse);
+    }
+    __syncthreads();
+    __shared__ int is_key_s;
+    if (threadIdx.x == 0) {
+      const int fsk = a.fsk[stream] + 1;
+      const bool key = trig > sp.aem_threshold || (sp.has_max_gop && fsk >= sp.max_gop);
+      int kind, ref;
+      if (key) {  // frame_select.py:119-125: key resets the accumulator
+        kind = 0;
+        ref = -1;
+        a.fsk[stream] = 0;
+        a.last_key[stream] = t;
+      } else if (sp.policy_keyframe) {
+        kind = 2;
+        ref = a.last_key[stream];
+        a.fsk[stream] = fsk;
+      } else {
+        kind = 1;
+        ref = t - 1;
+        a.fsk[stream] = fsk;
+      }
+      const long long o = (long long)stream * a.dss + t;
+      a.kind[o] = kind;
+      a.ref[o] = ref;
+      a.trigger[o] = trig;
+      // reference frame of the NEXT frame's motion search (pipeline.py:102-106)
+      if (a.ref_next)
+        a.ref_next[stream] = stream * a.frames_per_stream + (sp.policy_keyframe ? a.last_key[stream] : t);
+      is_key_s = key;
+    }
+    __syncthreads();
+    if (is_key_s)
+      for (int c = threadIdx.x; c < ncoarse; c += blockDim.x) acc[c] = 0.0;
+    __syncthreads();
+  }
+}
+
+int launch_decide(const DecideArgs& a, cudaStream_t st) {
+  const int ncoarse = a.sp.coarse_h * a.sp.coarse_w;
+  const long long nleaf = pairwise_leaf_count(ncoarse);
+  const size_t smem = (size_t)nleaf * (8 + 8 + 4) + 16;
+  if (smem > 200 * 1024) {
+    set_error("AEM grid of %d cells is too large for the on-chip mean", ncoarse);
+    return BMC_E_ARG;
+  }
+  cudaError_t e = cudaFuncSetAttribute(decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(decide)");
+  DecideArgs a2 = a;
+  a2.nleaf = nleaf;
+  decide_kernel<<<a.n_streams, kThreads, smem, st>>>(a2);
+  return cuda_status(cudaGetLastError(), "decide_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Motion compensation (propagate.py:17-55):
+//   out[y, x] = ref[clip(y + s*dy), clip(x + s*dx)] with (dx, dy) the MV of the
+// final block containing (y, x).  Key frames copy the injected key labels.
+// One thread produces 16 consecutive output bytes (one 16-byte store).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) predict_kernel(const PredictArgs a) {
+  const int stream = blockIdx.y;
+  const long long o = (long long)stream * a.kss + a.t;
+  const int kind = a.kind ? a.kind[o] : 1;
+  uint8_t* out = a.labels + stream * a.ss + a.t * a.fs;
+  const int groups_per_row = (a.W + 15) / 16;
+  const long long total = (long long)a.H * groups_per_row;
+  if (kind == 0) {
+    const uint8_t* src = a.key_labels + stream * a.ss + a.t * a.fs;
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+         g += (long long)gridDim.x * blockDim.x) {
+      const int y = (int)(g / groups_per_row), x0 = (int)(g % groups_per_row) * 16;
+      for (int x = x0; x < min(x0 + 16, a.W); ++x) out[(long long)y * a.W + x] = src[(long long)y * a.W + x];
+    }
+    return;
+  }
+  const int r = a.ref ? a.ref[o] : a.ref_fixed;
+  const uint8_t* src = a.labels + stream * a.ss + (long long)r * a.fs;
+  const int32_t* mv = a.mv + stream * a.mvss + a.t * a.mvfs;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int y = (int)(g / groups_per_row), x0 = (int)(g % groups_per_row) * 16;
+    const int gy = y / a.B;
+    uint32_t words[4] = {0, 0, 0, 0};
+    int gxc = -1, dx = 0, sy = 0;
+    const int n = min(16, a.W - x0);
+    for (int e = 0; e < n; ++e) {
+      const int x = x0 + e;
+      const int gx = x / a.B;
+      if (gx != gxc) {
+        gxc = gx;
+        const int c = gy * a.gw + gx;
+        dx = __ldg(mv + 2 * c) * a.scale;
+        const int dy = __ldg(mv + 2 * c + 1) * a.scale;
+        sy = min(max(y + dy, 0), a.H - 1);
+      }
+      const int sx = min(max(x + dx, 0), a.W - 1);
+      words[e >> 2] |= (uint32_t)src[(long long)sy * a.W + sx] << (8 * (e & 3));
+    }
+    uint8_t* dst = out + (long long)y * a.W + x0;
+    if (n == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(words[0], words[1], words[2], words[3]);
+    } else {
+      for (int e = 0; e < n; ++e) dst[e] = (uint8_t)(words[e >> 2] >> (8 * (e & 3)));
+    }
+  }
+}
+
+int launch_predict(const PredictArgs& a, int n_streams, cudaStream_t st) {
+  const long long total = (long long)a.H * ((a.W + 15) / 16);
+  long long bx = (total + kThreads - 1) / kThreads;
+  if (bx > 148 * 8) bx = 148 * 8;
+  if (bx < 1) bx = 1;
+  predict_kernel<<<dim3((unsigned)bx, n_streams), kThreads, 0, st>>>(a);
+  return cuda_status(cudaGetLastError(), "predict_kernel");
+}
+
+__global__ void predict_features_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int H, int W,
+                                        const int32_t* __restrict__ mv, int gw, int B, int scale) {
+  const long long total = (long long)C * H * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % W);
+    const int y = (int)((i / W) % H);
+    const long long c = i / ((long long)H * W);
+    const int cell = (y / B) * gw + (x / B);
+    const int sy = min(max(y + __ldg(mv + 2 * cell + 1) * scale, 0), H - 1);
+    const int sx = min(max(x + __ldg(mv + 2 * cell) * scale, 0), W - 1);
+    dst[i] = src[(c * H + sy) * W + sx];
+  }
+}
+
+int launch_predict_features(const float* src, float* dst, int C, int H, int W, const int32_t* mv, int gw, int B,
+                            int scale, cudaStream_t st) {
+  const long long total = (long long)C * H * W;
+  long long blocks = (total + kThreads - 1) / kThreads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  predict_features_kernel<<<(unsigned)blocks, kThreads, 0, st>>>(src, dst, C, H, W, mv, gw, B, scale);
+  return cuda_status(cudaGetLastError(), "predict_features_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// block_energy on arbitrary float64 arrays (fme.py:218-233).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) block_energy_kernel(const double* __restrict__ a,
+                                                                const double* __restrict__ b, long long n,
+                                                                long long nleaf, double lam, double tol,
+                                                                double* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double result;
+  __shared__ int cnt_s;
+  long long* leaf_lo = reinterpret_cast<long long*>(smem_raw);
+  double* leaf_val = reinterpret_cast<double*>(leaf_lo + nleaf);
+  int* leaf_len = reinterpret_cast<int*>(leaf_val + nleaf) + 1;
+  if (threadIdx.x == 0) cnt_s = 0;
+  auto diff = [&](long long i) { return fabs(__dsub_rn(a[i], b[i])); };
+  const double s = block_pairwise(diff, n, leaf_lo, leaf_len, leaf_val, &result);
+  int c = 0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) c += diff(i) > tol;
+  atomicAdd(&cnt_s, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double nd = (double)n;
+    // (1.0 - lam) * sad_norm + lam * sparsity  (fme.py:231-233)
+    *out = __dadd_rn(__dmul_rn(__dsub_rn(1.0, lam), __ddiv_rn(s, nd)), __dmul_rn(lam, __ddiv_rn((double)cnt_s, nd)));
+  }
+}
+
+int launch_block_energy(const double* a, const double* b, long long n, double lam, double tol, double* out,
+                        cudaStream_t st) {
+  const long long nleaf = pairwise_leaf_count(n);
+  const size_t smem = (size_t)nleaf * 20 + 16;
+  if (smem > 200 * 1024) {
+    set_error("block of %lld samples is too large for block_energy", n);
+    return BMC_E_ARG;
+  }
+  cudaError_t e = cudaFuncSetAttribute(block_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(block_energy)");
+  block_energy_kernel<<<1, kThreads, smem, st>>>(a, b, n, nleaf, lam, tol, out);
+  return cuda_status(cudaGetLastError(), "block_energy_kernel");
+}
+
+}  // namespace bmc

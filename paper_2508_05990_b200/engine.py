@@ -1,0 +1,219 @@
+"""Device-resident batched pipeline: S streams x T frames per step.
+
+This is the B200 replacement of the per-frame loop in ``run_sequence``
+(pipeline.py:97-141) minus CaBR.  One step is
+
+  pack (raw Bayer -> padded CFA planes)            bmc_pack_planes
+  ME for every frame pair, all levels              bmc_estimate_motion
+  3x3 MV refinement + energy re-evaluation         bmc_refine_mvs
+  AEM key-frame scan over the clip                 bmc_decide
+  label propagation chain (key copy / gather)      bmc_predict_labels x T
+
+all enqueued on one CUDA stream with no host synchronisation, so the whole
+step can be captured in a CUDA graph.  With the default "previous" reference
+policy ME/refine of all pairs of all streams run as ONE launch each (the pairs
+are independent); with "keyframe" the reference frame depends on earlier
+decisions, so ME/refine/decide run frame by frame, with the decide kernel
+writing the next frame's reference index straight into the ME index array.
+
+Device layouts (pair p of frame t >= 1 of stream s is p = (t-1)*S + s):
+  raw        (S, T, H, W)           uint8/uint16
+  planes     (S*T, P, pad_h, pitch) uint8/uint16
+  levels[L]  mv (pairs, gh, gw, 2) int32, energy f64, matched u8, evals i64
+  refined    mv (pairs, gh, gw, 2) int32, energy f64
+  decisions  kind/ref (S, T) int32, trigger (S, T) f64
+  labels     (S, T, Hl, Wl) uint8 (key_labels: same layout, key slots used)
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .config import PipelineConfig
+
+
+class ClipEngine:
+    def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, n_streams: int = 1,
+                 dtype=np.uint8, bayer: bool = True, label_hw=None):
+        torch = N.require_cuda()
+        if config.aem_statistic not in ("max", "mean"):
+            raise ValueError("statistic must be 'max' or 'mean'")
+        if config.reference_policy not in ("previous", "keyframe"):
+            raise ValueError("reference_policy must be 'previous' or 'keyframe'")
+        if n_frames < 1 or n_streams < 1:
+            raise ValueError("need at least one frame and one stream")
+        self.torch = torch
+        self.cfg = config
+        self.S, self.T, self.H, self.W = int(n_streams), int(n_frames), int(height), int(width)
+        self.bayer = bool(bayer)
+        self.scale = 2 if self.bayer else 1
+        tdt = torch.uint8 if np.dtype(dtype) == np.uint8 else torch.uint16
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.kind_code = N.KIND_BAYER if self.bayer else N.KIND_LUMA
+        self.params = N.make_params(self.kind_code, 1 if tdt == torch.uint8 else 2, self.H, self.W, config.fme)
+        p = self.params
+        lib = N.load()
+        S, T = self.S, self.T
+        self.raw = torch.zeros((S, T, self.H, self.W), dtype=tdt, device=self.dev)
+        self.planes = torch.empty(lib.bmc_plane_buffer_elems(ctypes.byref(p), S * T), dtype=tdt, device=self.dev)
+        self.n_pairs = S * (T - 1)
+        t = torch.arange(1, T, dtype=torch.int32, device=self.dev).repeat_interleave(S)
+        s = torch.arange(S, dtype=torch.int32, device=self.dev).repeat(T - 1)
+        self.cur_index = (s * T + t).contiguous()
+        self.ref_index_init = (s * T + t - 1).contiguous() if config.reference_policy == "previous" \
+            else (s * T).contiguous()
+        self.ref_index = self.ref_index_init.clone()
+        sizes = list(config.fme.block_sizes)
+        self.levels = [D.LevelBuffers(torch, self.dev, max(self.n_pairs, 1), p.pad_h // b, p.pad_w // b)
+                       for b in sizes]
+        fin = self.levels[-1]
+        self.b_final = sizes[-1]
+        self.gh, self.gw = fin.gh, fin.gw
+        self.mv_ref = torch.empty_like(fin.mv)
+        self.e_ref = torch.empty_like(fin.energy)
+        self.replaced = torch.empty(fin.energy.shape, dtype=torch.int32, device=self.dev)
+        coarse = sizes[0]
+        self.ch, self.cw = p.pad_h // coarse, p.pad_w // coarse
+        self.sp = N.select_params(self.gh, self.gw, coarse // self.b_final, self.ch, self.cw, config.aem_statistic,
+                                  config.reference_policy, config.max_gop, config.aem_threshold)
+        self.acc = torch.zeros((S, self.ch, self.cw), dtype=torch.float64, device=self.dev)
+        self.fsk = torch.zeros(S, dtype=torch.int32, device=self.dev)
+        self.last_key = torch.zeros(S, dtype=torch.int32, device=self.dev)
+        self.kind = torch.zeros((S, T), dtype=torch.int32, device=self.dev)
+        self.ref = torch.full((S, T), -1, dtype=torch.int32, device=self.dev)
+        self.trigger = torch.zeros((S, T), dtype=torch.float64, device=self.dev)
+        self.set_label_size(*(label_hw or (self.H, self.W)))
+        self.graph = None
+
+    # ------------------------------------------------------------------ buffers
+    def set_label_size(self, h: int, w: int) -> None:
+        B = self.b_final * self.scale
+        if self.gw * B < w or self.gh * B < h:
+            raise ValueError(f"motion field covers {self.gw * B}x{self.gh * B}, labels are {w}x{h}")
+        self.Hl, self.Wl = int(h), int(w)
+        self.labels = self.torch.zeros((self.S, self.T, h, w), dtype=self.torch.uint8, device=self.dev)
+        self.key_labels = self.torch.zeros_like(self.labels)
+        self.graph = None
+
+    def load_frames(self, frames, non_blocking: bool = False) -> None:
+        """Copy (S, T, H, W) or (T, H, W) frames (numpy / CPU or CUDA tensor) into the raw slot."""
+        src = frames
+        if isinstance(src, np.ndarray):
+            src = self.torch.from_numpy(np.ascontiguousarray(src))
+        self.raw.view(-1, self.H, self.W).copy_(src.reshape(-1, self.H, self.W), non_blocking=non_blocking)
+
+    # ------------------------------------------------------------------ stages
+    def _level_slice(self, lo: int, hi: int):
+        out = []
+        for lv in self.levels:
+            out.append(N.LevelOut(N.ptr(lv.mv[lo:hi]), N.ptr(lv.energy[lo:hi]), N.ptr(lv.matched[lo:hi]),
+                                  N.ptr(lv.evals[lo:hi])))
+        return (N.LevelOut * len(out))(*out)
+
+    def _reset_state(self) -> None:
+        self.acc.zero_()
+        self.fsk.zero_()
+        self.last_key.zero_()
+        self.kind.zero_()
+        self.ref.fill_(-1)
+        self.trigger.zero_()
+        if self.cfg.reference_policy == "keyframe":
+            self.ref_index.copy_(self.ref_index_init)
+
+    def _decide(self, t0: int, t1: int, ref_next=None) -> None:
+        cells = self.gh * self.gw
+        S = self.S
+        N.check(N.load().bmc_decide(
+            N.ptr(self.e_ref) - 8 * S * cells, S * cells, cells, S, t0, t1, ctypes.byref(self.sp),
+            N.ptr(self.acc), N.ptr(self.fsk), N.ptr(self.last_key), N.ptr(self.kind), N.ptr(self.ref),
+            N.ptr(self.trigger), self.T, ref_next, self.T, N.stream_handle()))
+
+    def motion(self) -> None:
+        """Pack + ME + refine + AEM decisions for every frame of every stream."""
+        lib = N.load()
+        p = self.params
+        st = N.stream_handle()
+        N.check(lib.bmc_pack_planes(N.ptr(self.raw), self.S * self.T, self.kind_code, ctypes.byref(p),
+                                    N.ptr(self.planes), st))
+        self._reset_state()
+        if self.T < 2:
+            return
+        if self.cfg.reference_policy == "previous":
+            arr = self._level_slice(0, self.n_pairs)
+            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), ctypes.byref(p), self.n_pairs,
+                                            N.ptr(self.cur_index), N.ptr(self.ref_index), arr, st))
+            self._refine(0, self.n_pairs)
+            self._decide(1, self.T)
+            return
+        S = self.S
+        for t in range(1, self.T):
+            lo, hi = (t - 1) * S, t * S
+            arr = self._level_slice(lo, hi)
+            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), ctypes.byref(p), S, N.ptr(self.cur_index[lo:hi]),
+                                            N.ptr(self.ref_index[lo:hi]), arr, st))
+            self._refine(lo, hi)
+            nxt = N.ptr(self.ref_index[hi:hi + S]) if t + 1 < self.T else None
+            self._decide(t, t + 1, nxt)
+
+    def _refine(self, lo: int, hi: int) -> None:
+        fin = self.levels[-1]
+        N.check(N.load().bmc_refine_mvs(
+            N.ptr(fin.mv[lo:hi]), N.ptr(fin.energy[lo:hi]), hi - lo, self.gh, self.gw, self.b_final,
+            int(self.cfg.deviation_threshold), N.ptr(self.planes), ctypes.byref(self.params),
+            N.ptr(self.cur_index[lo:hi]), N.ptr(self.ref_index[lo:hi]), N.ptr(self.mv_ref[lo:hi]),
+            N.ptr(self.e_ref[lo:hi]), N.ptr(self.replaced[lo:hi]), N.stream_handle()))
+
+    def predict(self) -> None:
+        """Label chain: key frames copy key_labels, others gather from their reference."""
+        lib = N.load()
+        st = N.stream_handle()
+        cells2 = self.gh * self.gw * 2
+        fs = self.Hl * self.Wl
+        for t in range(self.T):
+            N.check(lib.bmc_predict_labels(
+                N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, t, N.ptr(self.kind),
+                N.ptr(self.ref), 0, self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
+                self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale, st))
+
+    def step(self) -> None:
+        self.motion()
+        self.predict()
+
+    # ------------------------------------------------------------------ graphs
+    def capture(self) -> None:
+        """Capture one full step (motion + predict) as a CUDA graph."""
+        torch = self.torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step()  # warm-up: sets kernel attributes, builds tables
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        self.graph = g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    # ------------------------------------------------------------------ results
+    def decisions_host(self):
+        return self.kind.cpu().numpy(), self.ref.cpu().numpy(), self.trigger.cpu().numpy()
+
+    def level_host(self, level: int):
+        lv = self.levels[level]
+        return (lv.mv[:self.n_pairs].cpu().numpy(), lv.energy[:self.n_pairs].cpu().numpy(),
+                lv.matched[:self.n_pairs].cpu().numpy(), lv.evals[:self.n_pairs].cpu().numpy())
+
+    def refined_host(self):
+        return (self.mv_ref[:self.n_pairs].cpu().numpy(), self.e_ref[:self.n_pairs].cpu().numpy(),
+                self.replaced[:self.n_pairs].cpu().numpy())
+
+    def pair_index(self, s: int, t: int) -> int:
+        return (t - 1) * self.S + s
