@@ -80,10 +80,10 @@ int bmc_pack_planes(const void* raw, int n_frames, int kind, const bmc_fme_param
                     void* planes, void* stream);
 
 /* Hierarchical ME for n_pairs frame pairs (cur_index[i], ref_index[i] index
- * frames of `planes`; both are DEVICE int32 arrays so a device-side scheduler
- * can pick references).  Replaces fme.estimate_motion (fme.py:324-392),
+ * the n_frames frames of `planes`; both are DEVICE int32 arrays so a
+ * device-side scheduler can pick references).  Replaces fme.estimate_motion (fme.py:324-392),
  * including _search_block (:294-316) and _stage_candidates (:236-268). */
-int bmc_estimate_motion(const void* planes, const bmc_fme_params* p, int n_pairs,
+int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* p, int n_pairs,
                         const int32_t* cur_index, const int32_t* ref_index,
                         bmc_level_out* levels, void* stream);
 

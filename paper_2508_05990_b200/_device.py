@@ -66,7 +66,7 @@ def alloc_levels(ps: PlaneSet, n_pairs: int):
 def run_estimate(ps: PlaneSet, cur_index, ref_index, levels, stream=None) -> None:
     """Launch hierarchical ME for len(cur_index) pairs (device int32 index tensors)."""
     arr = (N.LevelOut * len(levels))(*[lv.as_c() for lv in levels])
-    N.check(N.load().bmc_estimate_motion(N.ptr(ps.planes), ctypes.byref(ps.params), int(cur_index.numel()),
+    N.check(N.load().bmc_estimate_motion(N.ptr(ps.planes), ps.n_frames, ctypes.byref(ps.params), int(cur_index.numel()),
                                          N.ptr(cur_index), N.ptr(ref_index), arr, N.stream_handle(stream)))
 
 

@@ -56,7 +56,7 @@ _SIGNATURES = {
                                        ctypes.POINTER(i32), f64, f64, f64, f64]),
     "bmc_plane_buffer_elems": (ctypes.c_size_t, [ctypes.POINTER(FmeParams), ctypes.c_int]),
     "bmc_pack_planes": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(FmeParams), vp, vp]),
-    "bmc_estimate_motion": (ctypes.c_int, [vp, ctypes.POINTER(FmeParams), ctypes.c_int, vp, vp,
+    "bmc_estimate_motion": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(FmeParams), ctypes.c_int, vp, vp,
                                            ctypes.POINTER(LevelOut), vp]),
     "bmc_search_stage": (ctypes.c_int, [vp, vp, ctypes.POINTER(FmeParams)] + [ctypes.c_int] * 7 + [vp, vp, vp, vp]),
     "bmc_block_energy_f64": (ctypes.c_int, [vp, vp, i64, f64, f64, vp, vp]),

@@ -159,12 +159,12 @@ int bmc_pack_planes(const void* raw, int n_frames, int kind, const bmc_fme_param
   return launch_pack(raw, n_frames, kind, *p, planes, (cudaStream_t)stream);
 }
 
-int bmc_estimate_motion(const void* planes, const bmc_fme_params* p, int n_pairs, const int32_t* cur_index,
-                        const int32_t* ref_index, bmc_level_out* levels, void* stream) {
+int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* p, int n_pairs,
+                        const int32_t* cur_index, const int32_t* ref_index, bmc_level_out* levels, void* stream) {
   int rc = check_params(p);
   if (rc) return rc;
-  if (!planes || !cur_index || !ref_index || !levels || n_pairs < 0) {
-    set_error("NULL argument");
+  if (!planes || !cur_index || !ref_index || !levels || n_pairs < 0 || n_frames < 1) {
+    set_error("NULL argument or empty plane buffer");
     return BMC_E_ARG;
   }
   if (n_pairs == 0) return BMC_OK;
@@ -174,35 +174,54 @@ int bmc_estimate_motion(const void* planes, const bmc_fme_params* p, int n_pairs
     set_error("could not build the uint16 normalisation table");
     return BMC_E_CUDA;
   }
+  // Which stages need a launch: a range-0 stage after a searched stage picks
+  // the same candidate again (same window, same energy) and only adds 1 to
+  // the candidate count (fme.py:306-315).
+  int launched[3], extra[3] = {0, 0, 0}, nl = 0;
+  for (int s = 0; s < 3; ++s) {
+    if (p->stage_range[s] == 0 && nl > 0)
+      ++extra[launched[nl - 1]];
+    else
+      launched[nl++] = s;
+  }
   for (int L = 0; L < p->n_levels; ++L) {
     const int b = p->block_sizes[L];
-    LevelArgs a;
-    std::memset(&a, 0, sizeof a);
-    rc = plan_level(a.plan, *p, b);
+    rc = cuda_status(cudaMemsetAsync(levels[L].evals, 0, sizeof(unsigned long long) * n_pairs, st), "memset evals");
     if (rc) return rc;
-    a.planes = planes;
-    a.prm = *p;
-    a.cur_index = cur_index;
-    a.ref_index = ref_index;
-    a.level = L;
-    a.final_level = L == p->n_levels - 1;
-    a.b = b;
-    a.gw = p->pad_w / b;
-    a.gh = p->pad_h / b;
-    if (L) {
-      a.parent_mv = levels[L - 1].mv;
-      a.parent_e = levels[L - 1].energy;
-      a.parent_matched = levels[L - 1].matched;
+    for (int k = 0; k < nl; ++k) {
+      const int s = launched[k];
+      StageLaunch a;
+      std::memset(&a, 0, sizeof a);
+      rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true);
+      if (rc) return rc;
+      a.planes = planes;
+      a.ref_planes = planes;
+      a.prm = *p;
+      a.cur_index = cur_index;
+      a.ref_index = ref_index;
+      a.level = L;
+      a.final_level = L == p->n_levels - 1;
+      a.b = b;
+      a.gw = p->pad_w / b;
+      a.gh = p->pad_h / b;
+      a.first = k == 0;
+      a.last = k == nl - 1;
+      a.r = p->stage_range[s];
+      a.s = p->stage_step[s];
+      a.extra_evals = extra[s];
+      if (L) {
+        a.parent_mv = levels[L - 1].mv;
+        a.parent_e = levels[L - 1].energy;
+        a.parent_matched = levels[L - 1].matched;
+      }
+      a.mv = levels[L].mv;
+      a.energy = levels[L].energy;
+      a.matched = levels[L].matched;
+      a.evals = levels[L].evals;
+      a.tab16 = tab16;
+      rc = launch_fme_stage(a, n_frames, n_frames, dim3(a.gw * a.gh, n_pairs), st);
+      if (rc) return rc;
     }
-    a.mv = levels[L].mv;
-    a.energy = levels[L].energy;
-    a.matched = levels[L].matched;
-    a.evals = levels[L].evals;
-    a.tab16 = tab16;
-    rc = cuda_status(cudaMemsetAsync(a.evals, 0, sizeof(unsigned long long) * n_pairs, st), "memset evals");
-    if (rc) return rc;
-    rc = launch_fme_level(a, n_pairs, st);
-    if (rc) return rc;
   }
   return BMC_OK;
 }
@@ -224,24 +243,28 @@ int bmc_search_stage(const void* cur_planes, const void* ref_planes, const bmc_f
     set_error("search range must be >= 0 and step >= 1");
     return BMC_E_ARG;
   }
-  const double* tab16 = p->elem_bytes == 2 ? tab16_for_current_device() : nullptr;
-  StageArgs a;
+  StageLaunch a;
   std::memset(&a, 0, sizeof a);
-  a.cur = cur_planes;
-  a.ref = ref_planes;
+  // arbitrary origins: plain-load staging (TMA tiles need 16-byte aligned starts)
+  rc = plan_stage(a.plan, *p, block_size, search_range, step, false);
+  if (rc) return rc;
+  a.planes = cur_planes;
+  a.ref_planes = ref_planes;
   a.prm = *p;
-  a.ox = origin_x;
-  a.oy = origin_y;
   a.b = block_size;
-  a.cx = center_x;
-  a.cy = center_y;
+  a.first = a.last = 1;
   a.r = search_range;
   a.s = step;
+  a.single = 1;
+  a.ox = origin_x;
+  a.oy = origin_y;
+  a.cx = center_x;
+  a.cy = center_y;
   a.mv = mv_out;
   a.energy = energy_out;
-  a.nvalid = n_valid_out;
-  a.tab16 = tab16;
-  return launch_stage(a, (cudaStream_t)stream);
+  a.nvalid_out = n_valid_out;
+  a.tab16 = p->elem_bytes == 2 ? tab16_for_current_device() : nullptr;
+  return launch_fme_stage(a, 1, 1, dim3(1, 1), (cudaStream_t)stream);
 }
 
 int bmc_block_energy_f64(const double* cur_block, const double* ref_block, int64_t n, double lam,

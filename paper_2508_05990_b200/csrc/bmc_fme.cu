@@ -3,24 +3,39 @@
 // Replaces fme.estimate_motion / _search_block / _stage_candidates
 // (fme.py:236-392) and search_stage (fme.py:271-291).
 //
-// One CTA searches one block of one frame pair through the three chained
-// stages (fme.py:306-315).  Per stage:
-//   A. integer screening: the reference window (candidate grid + block halo) is
-//      staged into shared memory once per CTA as EPW/gcd(step,EPW) copies, each
-//      pre-shifted by a sub-word element offset, so every candidate row reads
-//      aligned 32-bit words (no SHF/PRMT on the hot loop; those share the ALU
-//      pipe with VABSDIFF4 and would halve throughput).  A thread owns TY
-//      vertically adjacent candidates of one column and slides a TY-row
-//      register window down the block, so each loaded ref word feeds TY packed
-//      SAD instructions (VABSDIFF4.U8.ACC for uint8, VIMNMX.U16x2+IDP.2A for
-//      uint16); the current block row is a broadcast LDS.128.
-//   B. exact selection: E >= (1-lam)*SAD/(s*n) because the sparsity term is
-//      >= 0, so only candidates whose integer lower bound does not exceed the
-//      exact energy of the min-SAD candidate (+1e-11 slack, far above the
-//      ~1e-15 float error) can win.  Those are replayed in float64 in numpy's
-//      pairwise order (bmc_internal.cuh) and the first minimum in canonical
-//      dy-major order wins (np.argmin, fme.py:266).
+// One launch per (level, search stage); one CTA per (frame pair, block).  The
+// three chained stages of a block (fme.py:306-315) communicate through the
+// level's mv/energy arrays; stages with range 0 after a searched stage select
+// the same candidate again and are folded into the candidate count on the
+// host (no launch).  Per stage:
+//
+//   staging  one TMA box (cp.async.bulk.tensor.3d) brings the reference window
+//            (candidate grid + block halo, all staged planes) into shared
+//            memory and a second box the current block; the tensor map's
+//            out-of-bounds zero fill covers frame borders (those windows only
+//            belong to invalid candidates).  No per-word address math.
+//   A        integer screening.  A thread owns TY vertically adjacent
+//            candidates of one column (+ one plane): it slides a TY-row
+//            register window down the block so every loaded reference word
+//            feeds TY packed SAD instructions (VABSDIFF4.U8.ACC for uint8;
+//            VIMNMX.U16x2 x2 + IDP.2A for uint16).  Sub-word candidate offsets
+//            cost one SHF per loaded word (amortised over TY uses); the current
+//            block row is a broadcast LDS.128.  Partial SADs of the planes meet
+//            in a shared-memory array.
+//   B        exact selection.  E >= (1-lam)*SAD/(s*n) because the sparsity
+//            term is >= 0, so only candidates whose integer lower bound does
+//            not exceed the exact energy of the min-SAD candidate (+1e-11, far
+//            above the ~1e-15 float error) can win.  They are replayed in
+//            float64 in numpy's pairwise order (bmc_internal.cuh); the first
+//            minimum in canonical dy-major order wins (np.argmin, fme.py:266).
+//            A min SAD of 0 has E == 0 exactly and wins outright (lam < 1).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
 
 #include "bmc_internal.cuh"
 #include "bmc_launch.cuh"
@@ -29,20 +44,24 @@ namespace bmc {
 
 constexpr double kScreenEps = 1e-11;
 
+// ---------------------------------------------------------------------------
+// shared-memory carve-up
+// ---------------------------------------------------------------------------
 struct SmemLayout {
-  double* tab;
-  unsigned long long* red64;
-  double* best_e;
-  int* best_k;
-  int* misc;
-  double* miscd;
-  uint32_t* sad;
-  int* klist;
-  uint32_t* cur;
-  uint32_t* ref;
+  double* tab;                 // fl(v/255) for uint8
+  unsigned long long* red64;   // [kWarps]
+  double* best_e;              // [kWarps]
+  int* best_k;                 // [kWarps]
+  int* misc;                   // [16]
+  double* miscd;               // [4]
+  unsigned long long* bar;     // mbarrier
+  uint32_t* sad;               // [nmax]
+  int* klist;                  // [nmax]
+  uint32_t* cur;               // [pg][b][cbw_words]
+  uint32_t* win;               // [pg][hwin][bw_words]
 };
 
-__device__ __forceinline__ SmemLayout carve(unsigned char* base, const SearchPlan& pl) {
+__device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan& pl) {
   SmemLayout L;
   L.tab = reinterpret_cast<double*>(base);
   unsigned char* p = base + 256 * sizeof(double);
@@ -56,101 +75,104 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const SearchPla
   p += 16 * 4;
   L.miscd = reinterpret_cast<double*>(p);
   p += 4 * 8;
-  p = base + ((p - base + 15) & ~15);
-  L.sad = reinterpret_cast<uint32_t*>(p);
-  p += ((pl.nmax * 4 + 15) & ~15);
-  L.klist = reinterpret_cast<int*>(p);
-  p += ((pl.nmax * 4 + 15) & ~15);
-  L.cur = reinterpret_cast<uint32_t*>(p);
-  p += pl.pg * pl.cur_words * 4;
-  L.ref = reinterpret_cast<uint32_t*>(p);
+  L.bar = reinterpret_cast<unsigned long long*>(p);
+  L.sad = reinterpret_cast<uint32_t*>(base + pl.off_sad);
+  L.klist = reinterpret_cast<int*>(base + pl.off_klist);
+  L.cur = reinterpret_cast<uint32_t*>(base + pl.off_cur);
+  L.win = reinterpret_cast<uint32_t*>(base + pl.off_win);
   return L;
 }
 
-// Frame geometry + arithmetic constants for one (cur, ref) pair.
+// ---------------------------------------------------------------------------
+// TMA helpers (inline PTX)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// per-CTA context
+// ---------------------------------------------------------------------------
 template <typename Elem>
 struct PairCtx {
-  const Elem* cur;  // plane 0 of the current frame
-  const Elem* ref;  // plane 0 of the reference frame
+  const Elem* cur;  // plane 0 of the current frame (global)
+  const Elem* ref;  // plane 0 of the reference frame (global)
+  int cur_z, ref_z; // first plane index of each frame in the tensor map's z dimension
   int pitch;
   long long plane_stride;
-  int frame_h, frame_w;  // candidate validity bounds (padded plane dims)
+  int frame_h, frame_w;  // candidate validity bounds
   int P;
   int max_value;
-  const double* tab;  // fl(v/s) lookup
+  const double* tab;
   double tol, lam, oml;
 };
 
 struct StageGeom {
-  int r, s, G, ty, ncg;
+  int r, s, G, ncg;
   int cx, cy;
-  int wx0, wy0, wwin, hwin;
-  int cstep, ncopies, row_words, cs;
+  int wx0, wy0;  // window origin in plane coordinates
+  int tx0;       // x of the staged box (wx0 rounded down to 16 bytes for TMA)
+  int d;         // wx0 - tx0: element offset of the window inside each staged row
 };
-
-template <int EPW>
-__device__ __forceinline__ StageGeom make_geom(int ox, int oy, int b, int cx, int cy, int r, int s, int ty) {
-  StageGeom g;
-  g.r = r;
-  g.s = s;
-  g.G = 2 * r + 1;
-  g.ty = ty;
-  g.ncg = (g.G + ty - 1) / ty;
-  g.cx = cx;
-  g.cy = cy;
-  g.wx0 = ox + cx - r * s;
-  g.wy0 = oy + cy - r * s;
-  g.wwin = 2 * r * s + b;
-  g.hwin = g.wwin;
-  int gs = s % EPW == 0 ? EPW : (s % 2 == 0 ? 2 : 1);
-  if (gs > EPW) gs = EPW;
-  g.cstep = gs;
-  g.ncopies = (g.G == 1) ? 1 : EPW / gs;
-  g.row_words = (g.wwin + EPW - 1) / EPW;
-  int cs = g.hwin * g.row_words;
-  cs += ((8 - (cs & 31)) + 32) & 31;  // copy blocks start 8 banks apart
-  g.cs = cs;
-  return g;
-}
 
 __device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
-// Stage `npl` planes of the ref window (all alignment copies) and of the
-// current block into shared memory.  `cur0`/`ref0` point at the first staged
-// plane.  Out-of-frame rows/words are clamped to in-bounds memory: they only
-// ever feed candidates that are invalid.  (Plain scalar arguments on purpose:
-// an earlier version that took a copied context struct was miscompiled at -O3,
-// losing the high word of the 64-bit plane stride.)
+// Fallback staging with plain loads (windows larger than a TMA box).
 template <typename Elem>
-__device__ void stage_planes(const SmemLayout& L, const Elem* __restrict__ cur0, const Elem* __restrict__ ref0,
-                             int pitch, long long plane_stride, int frame_h, const StageGeom& g, int ox, int oy,
-                             int b, int npl, const SearchPlan& pl) {
+__device__ void stage_ldg(const SmemLayout& L, const Elem* __restrict__ cur0, const Elem* __restrict__ ref0,
+                          int pitch, long long plane_stride, int frame_h, const StageGeom& g, int ox, int oy, int b,
+                          int npl, const StagePlan& pl) {
   constexpr int EPW = 4 / sizeof(Elem);
   constexpr int SH = 8 * sizeof(Elem);
+  const int bww = pl.bw / EPW;
   const int row_max_w = pitch / EPW - 1;
-  const int per_copy = g.hwin * g.row_words;
-  const int total = npl * g.ncopies * per_copy;
+  const int total = npl * pl.hwin * bww;
   for (int idx = threadIdx.x; idx < total; idx += kThreads) {
-    int t = idx;
-    const int w = t % g.row_words;
-    t /= g.row_words;
-    const int row = t % g.hwin;
-    t /= g.hwin;
-    const int sl = t % g.ncopies;
-    const int pp = t / g.ncopies;
+    const int w = idx % bww;
+    const int row = (idx / bww) % pl.hwin;
+    const int pp = idx / (bww * pl.hwin);
     const int gy = min(max(g.wy0 + row, 0), frame_h - 1);
-    const int gx = g.wx0 + w * EPW + sl * g.cstep;
+    const int gx = g.wx0 + w * EPW;
     const int gw0 = floor_div(gx, EPW);
     const int sh = gx - gw0 * EPW;
     const uint32_t* row32 =
         reinterpret_cast<const uint32_t*>(ref0 + (long long)pp * plane_stride + (long long)gy * pitch);
-    const int w0 = min(max(gw0, 0), row_max_w);
-    const int w1 = min(max(gw0 + 1, 0), row_max_w);
-    const uint32_t lo = __ldg(row32 + w0);
-    const uint32_t v = sh ? __funnelshift_r(lo, __ldg(row32 + w1), sh * SH) : lo;
-    L.ref[pp * pl.ref_words + sl * g.cs + row * g.row_words + w] = v;
+    const uint32_t lo = __ldg(row32 + min(max(gw0, 0), row_max_w));
+    const uint32_t v = sh ? __funnelshift_r(lo, __ldg(row32 + min(max(gw0 + 1, 0), row_max_w)), sh * SH) : lo;
+    L.win[(pp * pl.hwin + row) * bww + w] = v;
   }
-  const int cw = b / EPW;
+  const int cbw = pl.cbw / EPW, cw = b / EPW;
   const int ctot = npl * b * cw;
   for (int idx = threadIdx.x; idx < ctot; idx += kThreads) {
     const int w = idx % cw;
@@ -163,14 +185,8 @@ __device__ void stage_planes(const SmemLayout& L, const Elem* __restrict__ cur0,
     const int sh = gx - gw0 * EPW;
     const uint32_t lo = __ldg(row32 + gw0);
     const uint32_t v = sh ? __funnelshift_r(lo, __ldg(row32 + gw0 + 1), sh * SH) : lo;
-    L.cur[pp * pl.cur_words + row * cw + w] = v;
+    L.cur[(pp * b + row) * cbw + w] = v;
   }
-}
-
-template <int CW>
-__device__ __forceinline__ void load_words(uint32_t (&dst)[CW], const uint32_t* src) {
-#pragma unroll
-  for (int w = 0; w < CW; ++w) dst[w] = src[w];
 }
 
 template <int CW>
@@ -184,16 +200,34 @@ __device__ __forceinline__ void load_cur(uint32_t (&dst)[CW], const uint32_t* sr
   }
 }
 
-// Phase A: integer SAD of every (candidate, staged plane) into L.sad (atomics
-// merge plane groups and column chunks).
-template <typename Elem, int CW, int TY>
-__device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int npl, const SearchPlan& pl) {
+// One reference row of CW words starting `sh` bits into word src[0].
+template <int CW, bool SHIFT>
+__device__ __forceinline__ void load_row(uint32_t (&dst)[CW], const uint32_t* src, int sh) {
+  if constexpr (SHIFT) {
+    uint32_t w[CW + 1];
+#pragma unroll
+    for (int q = 0; q <= CW; ++q) w[q] = src[q];
+#pragma unroll
+    for (int q = 0; q < CW; ++q) dst[q] = __funnelshift_r(w[q], w[q + 1], sh);
+  } else {
+#pragma unroll
+    for (int q = 0; q < CW; ++q) dst[q] = src[q];
+  }
+}
+
+// Phase A: integer SAD of every (candidate column, TY-row group, chunk, staged
+// plane) item; partial sums meet in L.sad via shared atomics.
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int npl, const StagePlan& pl,
+                          int coff_w) {
   constexpr int EPW = 4 / sizeof(Elem);
-  const int curw = b / EPW;
-  const int cpr = curw / CW;
+  const int bww = pl.bw / EPW;
+  const int cbw = pl.cbw / EPW;
+  const int cpr = (b / EPW) / CW;
   const int items = g.G * g.ncg * cpr * npl;
   const int s = g.s;
   const int nrho = s < b ? s : b;
+  const int hmax = pl.hwin - 1;
   for (int it = threadIdx.x; it < items; it += kThreads) {
     int t = it;
     const int i = t % g.G;
@@ -202,32 +236,27 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
     t /= g.ncg;
     const int c = t % cpr;
     const int pp = t / cpr;
-    const int xo = i * s;
-    const int a = xo % EPW;
-    const uint32_t* R0 = L.ref + pp * pl.ref_words + (a / g.cstep) * g.cs + (xo / EPW) + c * CW;
-    const uint32_t* C0 = L.cur + pp * pl.cur_words + c * CW;
+    const int xo = g.d + i * s;
+    const int sh = (xo % EPW) * 8 * (int)sizeof(Elem);
+    const uint32_t* R0 = L.win + pp * pl.hwin * bww + (xo / EPW) + c * CW;
+    const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + c * CW;
     uint32_t acc[TY];
 #pragma unroll
     for (int j = 0; j < TY; ++j) acc[j] = 0;
-    const int hmax = g.hwin - 1;
     for (int rho = 0; rho < nrho; ++rho) {
       const int M = (b - 1 - rho) / s + 1;
       const int base = rho + gi * TY * s;
       uint32_t R[TY][CW];
 #pragma unroll
-      for (int k = 0; k < TY - 1; ++k) {
-        const int row = min(base + k * s, hmax);
-        load_words<CW>(R[k], R0 + row * g.row_words);
-      }
+      for (int k = 0; k < TY - 1; ++k) load_row<CW, SHIFT>(R[k], R0 + min(base + k * s, hmax) * bww, sh);
       for (int m0 = 0; m0 < M; m0 += TY) {
 #pragma unroll
         for (int k = 0; k < TY; ++k) {
           const int m = m0 + k;
           if (m < M) {
-            const int row = min(base + (m + TY - 1) * s, hmax);
-            load_words<CW>(R[(k + TY - 1) % TY], R0 + row * g.row_words);
+            load_row<CW, SHIFT>(R[(k + TY - 1) % TY], R0 + min(base + (m + TY - 1) * s, hmax) * bww, sh);
             uint32_t C[CW];
-            load_cur<CW>(C, C0 + (rho + m * s) * curw);
+            load_cur<CW>(C, C0 + (rho + m * s) * cbw);
 #pragma unroll
             for (int j = 0; j < TY; ++j) {
 #pragma unroll
@@ -245,71 +274,94 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   }
 }
 
-template <typename Elem, int CW>
-__device__ void sad_dispatch(const SmemLayout& L, const StageGeom& g, int b, int npl, const SearchPlan& pl) {
-  switch (g.ty) {
-    case 1: sad_items<Elem, CW, 1>(L, g, b, npl, pl); break;
-    case 2: sad_items<Elem, CW, 2>(L, g, b, npl, pl); break;
-    case 3: sad_items<Elem, CW, 3>(L, g, b, npl, pl); break;
-    case 4: sad_items<Elem, CW, 4>(L, g, b, npl, pl); break;
-    case 5: sad_items<Elem, CW, 5>(L, g, b, npl, pl); break;
-    case 6: sad_items<Elem, CW, 6>(L, g, b, npl, pl); break;
-    case 7: sad_items<Elem, CW, 7>(L, g, b, npl, pl); break;
-    case 8: sad_items<Elem, CW, 8>(L, g, b, npl, pl); break;
-    case 9: sad_items<Elem, CW, 9>(L, g, b, npl, pl); break;
-    case 10: sad_items<Elem, CW, 10>(L, g, b, npl, pl); break;
-    case 11: sad_items<Elem, CW, 11>(L, g, b, npl, pl); break;
-    default: sad_items<Elem, CW, 12>(L, g, b, npl, pl); break;
-  }
-}
-
 struct StageResult {
   int dx, dy;
   double energy;
   int nvalid;
 };
 
-__device__ __forceinline__ bool cand_valid(const StageGeom& g, int ox, int oy, int b, int fh, int fw, int k,
-                                           int& dx, int& dy) {
-  const int i = k % g.G, j = k / g.G;
+__device__ __forceinline__ bool cand_valid_ij(const StageGeom& g, int ox, int oy, int b, int fh, int fw, int i, int j,
+                                              int& dx, int& dy) {
   dx = g.cx + (i - g.r) * g.s;
   dy = g.cy + (j - g.r) * g.s;
   const int x = ox + dx, y = oy + dy;
   return x >= 0 && x <= fw - b && y >= 0 && y <= fh - b;
 }
 
-// One stage for one block; all threads of the CTA participate and receive the
-// result.  nvalid == 0 means every candidate window left the frame.
-template <typename Elem, int CW>
-__device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc, const SearchPlan& pl, int ox,
-                                    int oy, int b, int cx, int cy, int r, int s, int ty) {
-  constexpr int EPW = 4 / sizeof(Elem);
-  const StageGeom g = make_geom<EPW>(ox, oy, b, cx, cy, r, s, ty);
+template <typename Elem>
+__device__ __forceinline__ double exact_cand(const PairCtx<Elem>& pc, int ox, int oy, int b, int dx, int dy) {
+  const long long roff = (long long)(oy + dy) * pc.pitch + (ox + dx);
+  const long long coff = (long long)oy * pc.pitch + ox;
+  return exact_energy_warp<Elem>(pc.cur + coff, pc.ref + roff, pc.pitch, pc.plane_stride, b, pc.P, pc.tab, pc.tol,
+                                 pc.oml, pc.lam)
+      .energy;
+}
+
+// One stage for one block; all threads participate and receive the result.
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
+                                    const CUtensorMap* tm_win, const CUtensorMap* tm_cur, uint32_t& phase, int ox,
+                                    int oy, int b, int cx, int cy, int r, int s) {
+  StageGeom g;
+  g.r = r;
+  g.s = s;
+  g.G = 2 * r + 1;
+  g.ncg = (g.G + TY - 1) / TY;
+  g.cx = cx;
+  g.cy = cy;
+  g.wx0 = ox + cx - r * s;
+  g.wy0 = oy + cy - r * s;
+  // TMA tile loads need the box's inner start coordinate on a 16-byte boundary
+  constexpr int A16 = 16 / (int)sizeof(Elem);
+  g.tx0 = pl.use_tma ? g.wx0 - (((g.wx0 % A16) + A16) % A16) : g.wx0;
+  g.d = g.wx0 - g.tx0;
+  const int cx0 = pl.use_tma ? ox - (ox % A16) : ox;  // ox >= 0
+  const int coff_w = (ox - cx0) / (4 / (int)sizeof(Elem));
   const int N = g.G * g.G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = pc.P * b * b;
 
-  __syncthreads();  // previous users of smem are done
+  __syncthreads();  // previous users of smem are done; mbarrier init visible
   for (int k = tid; k < N; k += kThreads) L.sad[k] = 0;
   for (int p0 = 0; p0 < pc.P; p0 += pl.pg) {
     const int npl = min(pl.pg, pc.P - p0);
     if (p0) __syncthreads();
-    stage_planes<Elem>(L, pc.cur + (long long)p0 * pc.plane_stride, pc.ref + (long long)p0 * pc.plane_stride,
-                       pc.pitch, pc.plane_stride, pc.frame_h, g, ox, oy, b, npl, pl);
+    if (pl.use_tma) {
+      if (tid == 0) {
+        mbar_expect_tx(L.bar, (uint32_t)(pl.win_bytes + pl.cur_bytes));  // full boxes, OOB included
+        tma_load_3d(L.win, tm_win, g.tx0, g.wy0, pc.ref_z + p0, L.bar);
+        tma_load_3d(L.cur, tm_cur, cx0, oy, pc.cur_z + p0, L.bar);
+      }
+      mbar_wait(L.bar, phase);
+      phase ^= 1;
+    } else {
+      stage_ldg<Elem>(L, pc.cur + (long long)p0 * pc.plane_stride, pc.ref + (long long)p0 * pc.plane_stride, pc.pitch,
+                      pc.plane_stride, pc.frame_h, g, ox, oy, b, npl, pl);
+    }
     __syncthreads();
-    sad_dispatch<Elem, CW>(L, g, b, npl, pl);
+    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w);
   }
   __syncthreads();
 
-  // first min SAD among valid candidates (key = sad<<32 | k) and valid count
+  // pass 1: first minimum SAD among valid candidates (key = sad<<32 | k), valid count
   unsigned long long best = ~0ull;
   int nvalid = 0;
-  for (int k = tid; k < N; k += kThreads) {
-    int dx, dy;
-    if (cand_valid(g, ox, oy, b, pc.frame_h, pc.frame_w, k, dx, dy)) {
-      ++nvalid;
-      const unsigned long long key = ((unsigned long long)L.sad[k] << 32) | (unsigned)k;
-      best = key < best ? key : best;
+  {
+    int i = tid % g.G, j = tid / g.G;
+    const int di = kThreads % g.G, dj = kThreads / g.G;
+    for (int k = tid; k < N; k += kThreads) {
+      int dx, dy;
+      if (cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, i, j, dx, dy)) {
+        ++nvalid;
+        const unsigned long long key = ((unsigned long long)L.sad[k] << 32) | (unsigned)k;
+        best = key < best ? key : best;
+      }
+      i += di;
+      j += dj;
+      if (i >= g.G) {
+        i -= g.G;
+        ++j;
+      }
     }
   }
   for (int m = 16; m; m >>= 1) {
@@ -344,18 +396,19 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   }
   const int m0 = L.misc[0];
   const unsigned sad0 = (unsigned)L.misc[2];
-
-  // exact energy of the min-SAD candidate (S = 0 => E = 0 exactly).
+  if (sad0 == 0 && pc.oml > 0.0) {
+    // S == 0 gives E == 0.0 exactly; any earlier candidate has S > 0 and,
+    // with (1-lam) > 0, E > 0.  The first zero-SAD candidate wins.
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, res.dx, res.dy);
+    res.energy = 0.0;
+    return res;
+  }
   if (warp == 0) {
     double e0 = 0.0;
     if (sad0 != 0) {
       int dx, dy;
-      cand_valid(g, ox, oy, b, pc.frame_h, pc.frame_w, m0, dx, dy);
-      const long long roff = (long long)(oy + dy) * pc.pitch + (ox + dx);
-      const long long coff = (long long)oy * pc.pitch + ox;
-      e0 = exact_energy_warp<Elem>(pc.cur + coff, pc.ref + roff, pc.pitch, pc.plane_stride, b, pc.P, pc.tab,
-                                   pc.tol, pc.oml, pc.lam)
-               .energy;
+      cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, dx, dy);
+      e0 = exact_cand<Elem>(pc, ox, oy, b, dx, dy);
     }
     if (lane == 0) L.miscd[0] = e0;
   }
@@ -363,11 +416,21 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   const double e0 = L.miscd[0];
   const double bound = e0 + kScreenEps;
   const double unit = (double)pc.max_value * (double)n;
-  for (int k = tid; k < N; k += kThreads) {
-    int dx, dy;
-    if (k != m0 && cand_valid(g, ox, oy, b, pc.frame_h, pc.frame_w, k, dx, dy)) {
-      const double lb = pc.oml * ((double)L.sad[k] / unit);
-      if (lb <= bound) L.klist[atomicAdd(&L.misc[3], 1)] = k;
+  {
+    int i = tid % g.G, j = tid / g.G;
+    const int di = kThreads % g.G, dj = kThreads / g.G;
+    for (int k = tid; k < N; k += kThreads) {
+      int dx, dy;
+      if (k != m0 && cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, i, j, dx, dy)) {
+        const double lb = pc.oml * ((double)L.sad[k] / unit);
+        if (lb <= bound) L.klist[atomicAdd(&L.misc[3], 1)] = k;
+      }
+      i += di;
+      j += dj;
+      if (i >= g.G) {
+        i -= g.G;
+        ++j;
+      }
     }
   }
   __syncthreads();
@@ -377,12 +440,8 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   for (int e = warp; e < nk; e += kWarps) {
     const int k = L.klist[e];
     int dx, dy;
-    cand_valid(g, ox, oy, b, pc.frame_h, pc.frame_w, k, dx, dy);
-    const long long roff = (long long)(oy + dy) * pc.pitch + (ox + dx);
-    const long long coff = (long long)oy * pc.pitch + ox;
-    const double ek = exact_energy_warp<Elem>(pc.cur + coff, pc.ref + roff, pc.pitch, pc.plane_stride, b, pc.P,
-                                              pc.tab, pc.tol, pc.oml, pc.lam)
-                          .energy;
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, k % g.G, k / g.G, dx, dy);
+    const double ek = exact_cand<Elem>(pc, ox, oy, b, dx, dy);
     if (ek < be || (ek == be && k < bk)) {
       be = ek;
       bk = k;
@@ -407,226 +466,301 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   }
   __syncthreads();
   const int kw = L.misc[4];
-  cand_valid(g, ox, oy, b, pc.frame_h, pc.frame_w, kw, res.dx, res.dy);
+  cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, kw % g.G, kw / g.G, res.dx, res.dy);
   res.energy = L.miscd[1];
   return res;
 }
 
-template <typename Elem>
-__device__ void init_table(const SmemLayout& L, PairCtx<Elem>& pc, const double* gtab) {
+// ---------------------------------------------------------------------------
+// the stage kernel
+// ---------------------------------------------------------------------------
+template <typename Elem, int CW, int TY, bool SHIFT>
+__global__ void __launch_bounds__(kThreads, 2)
+    fme_stage_kernel(const __grid_constant__ CUtensorMap tm_win, const __grid_constant__ CUtensorMap tm_cur,
+                     const StageLaunch a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const SmemLayout L = carve(smem_raw, a.plan);
+  const bmc_fme_params& p = a.prm;
+  const int b = a.b;
+  int pair = 0, gx = 0, gy = 0, ox, oy, sx = 0, sy = 0;
+  long long cell = 0;
+  if (a.single) {
+    ox = a.ox;
+    oy = a.oy;
+    sx = a.cx;
+    sy = a.cy;
+  } else {
+    const int blk = blockIdx.x;
+    pair = blockIdx.y;
+    gx = blk % a.gw;
+    gy = blk / a.gw;
+    cell = (long long)pair * a.gw * a.gh + blk;
+    ox = gx * b;
+    oy = gy * b;
+    if (a.level > 0) {
+      const int pgw = a.gw / 2, pgh = a.gh / 2;
+      const long long pcell = (long long)pair * pgw * pgh + (gy / 2) * pgw + (gx / 2);
+      if (a.parent_matched[pcell]) {  // inherited: copy the parent (fme.py:352-362)
+        if (a.first && threadIdx.x == 0) {
+          a.mv[2 * cell] = a.parent_mv[2 * pcell];
+          a.mv[2 * cell + 1] = a.parent_mv[2 * pcell + 1];
+          a.energy[cell] = a.parent_e[pcell];
+          a.matched[cell] = 1;
+        }
+        return;
+      }
+      if (a.first) {
+        sx = a.parent_mv[2 * pcell];
+        sy = a.parent_mv[2 * pcell + 1];
+      }
+    }
+    if (!a.first) {
+      sx = a.mv[2 * cell];
+      sy = a.mv[2 * cell + 1];
+    }
+  }
+  PairCtx<Elem> pc;
+  const int cur_f = a.single ? 0 : a.cur_index[pair];
+  const int ref_f = a.single ? 0 : a.ref_index[pair];
+  pc.cur = reinterpret_cast<const Elem*>(a.planes) + (long long)cur_f * p.frame_stride;
+  pc.ref = reinterpret_cast<const Elem*>(a.ref_planes) + (long long)ref_f * p.frame_stride;
+  pc.cur_z = cur_f * p.planes;
+  pc.ref_z = ref_f * p.planes;
+  pc.pitch = p.pitch;
+  pc.plane_stride = p.plane_stride;
+  pc.frame_h = a.single ? p.real_h : p.pad_h;  // search_stage works on unpadded planes (fme.py:279-284)
+  pc.frame_w = a.single ? p.real_w : p.pad_w;
+  pc.P = p.planes;
+  pc.max_value = p.max_value;
+  pc.tol = p.sparsity_tolerance;
+  pc.lam = p.lam;
+  pc.oml = p.one_minus_lam;
   if (sizeof(Elem) == 1) {
-    for (int v = threadIdx.x; v < 256; v += kThreads) L.tab[v] = __ddiv_rn((double)v, (double)pc.max_value);
+    for (int v = threadIdx.x; v < 256; v += kThreads) L.tab[v] = __ddiv_rn((double)v, (double)p.max_value);
     pc.tab = L.tab;
   } else {
-    pc.tab = gtab;
+    pc.tab = a.tab16;
   }
-}
-
-template <typename Elem, int CW>
-__global__ void __launch_bounds__(kThreads, 2) fme_level_kernel(const LevelArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const SmemLayout L = carve(smem_raw, a.plan);
-  const int blk = blockIdx.x;
-  const int pair = blockIdx.y;
-  const int gx = blk % a.gw, gy = blk / a.gw;
-  const long long cell = (long long)pair * a.gw * a.gh + blk;
-  const int b = a.b;
-  int sx = 0, sy = 0;
-  if (a.level > 0) {
-    const int pgw = a.gw / 2, pgh = a.gh / 2;
-    const long long pcell = (long long)pair * pgw * pgh + (gy / 2) * pgw + (gx / 2);
-    sx = a.parent_mv[2 * pcell];
-    sy = a.parent_mv[2 * pcell + 1];
-    if (a.parent_matched[pcell]) {  // inherited (fme.py:357-362)
-      if (threadIdx.x == 0) {
-        a.mv[2 * cell] = sx;
-        a.mv[2 * cell + 1] = sy;
-        a.energy[cell] = a.parent_e[pcell];
-        a.matched[cell] = 1;
-      }
-      return;
-    }
-  }
-  const bmc_fme_params& p = a.prm;
-  PairCtx<Elem> pc;
-  pc.cur = reinterpret_cast<const Elem*>(a.planes) + (long long)a.cur_index[pair] * p.frame_stride;
-  pc.ref = reinterpret_cast<const Elem*>(a.planes) + (long long)a.ref_index[pair] * p.frame_stride;
-  pc.pitch = p.pitch;
-  pc.plane_stride = p.plane_stride;
-  pc.frame_h = p.pad_h;
-  pc.frame_w = p.pad_w;
-  pc.P = p.planes;
-  pc.max_value = p.max_value;
-  pc.tol = p.sparsity_tolerance;
-  pc.lam = p.lam;
-  pc.oml = p.one_minus_lam;
-  init_table<Elem>(L, pc, a.tab16);
-  const int ox = gx * b, oy = gy * b;
-  int mx = sx, my = sy;
-  double e = 0.0;
-  bool have = false;
-  unsigned long long evals = 0;
-  for (int st = 0; st < 3; ++st) {
-    const int r = p.stage_range[st], s = p.stage_step[st];
-    if (r == 0 && have) {  // single candidate == previous winner: same window, same energy
-      evals += 1;
-      continue;
-    }
-    StageResult res = stage_search<Elem, CW>(L, pc, a.plan, ox, oy, b, mx, my, r, s, a.plan.ty[st]);
-    if (res.nvalid == 0)  // fme.py:310-313
-      res = stage_search<Elem, CW>(L, pc, a.plan, ox, oy, b, 0, 0, r, s, a.plan.ty[st]);
-    mx = res.dx;
-    my = res.dy;
-    e = res.energy;
-    evals += res.nvalid;
-    have = true;
-  }
-  if (threadIdx.x == 0) {
-    a.mv[2 * cell] = mx;
-    a.mv[2 * cell + 1] = my;
-    a.energy[cell] = e;
-    bool m;
-    if (a.final_level) {
-      const bool in_real = oy < p.real_h && ox < p.real_w;  // fme.py:380-384
-      m = !(e > p.refine_block_threshold && in_real);
-    } else {
-      m = e <= p.split_threshold;  // fme.py:386
-    }
-    a.matched[cell] = m ? 1 : 0;
-    atomicAdd(a.evals + pair, evals);
-  }
-}
-
-template <typename Elem, int CW>
-__global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const SmemLayout L = carve(smem_raw, a.plan);
-  const bmc_fme_params& p = a.prm;
-  PairCtx<Elem> pc;
-  pc.cur = reinterpret_cast<const Elem*>(a.cur);
-  pc.ref = reinterpret_cast<const Elem*>(a.ref);
-  pc.pitch = p.pitch;
-  pc.plane_stride = p.plane_stride;
-  pc.frame_h = p.real_h;  // search_stage works on unpadded planes (fme.py:279-284)
-  pc.frame_w = p.real_w;
-  pc.P = p.planes;
-  pc.max_value = p.max_value;
-  pc.tol = p.sparsity_tolerance;
-  pc.lam = p.lam;
-  pc.oml = p.one_minus_lam;
-  init_table<Elem>(L, pc, a.tab16);
-  const StageResult res = stage_search<Elem, CW>(L, pc, a.plan, a.ox, a.oy, a.b, a.cx, a.cy, a.r, a.s, a.plan.ty[0]);
-  if (threadIdx.x == 0) {
+  uint32_t phase = 0;
+  if (a.plan.use_tma && threadIdx.x == 0) mbar_init(L.bar, 1);
+  StageResult res = stage_search<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox, oy, b, sx, sy, a.r,
+                                                      a.s);
+  if (res.nvalid == 0)  // fme.py:310-313
+    res = stage_search<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox, oy, b, 0, 0, a.r, a.s);
+  if (threadIdx.x != 0) return;
+  if (a.single) {
     a.mv[0] = res.dx;
     a.mv[1] = res.dy;
     a.energy[0] = res.energy;
-    a.nvalid[0] = res.nvalid;
+    a.nvalid_out[0] = res.nvalid;
+    return;
   }
+  a.mv[2 * cell] = res.dx;
+  a.mv[2 * cell + 1] = res.dy;
+  a.energy[cell] = res.energy;
+  if (a.last) {
+    bool m;
+    if (a.final_level) {
+      const bool in_real = oy < p.real_h && ox < p.real_w;  // fme.py:377-384
+      m = !(res.energy > p.refine_block_threshold && in_real);
+    } else {
+      m = res.energy <= p.split_threshold;  // fme.py:386
+    }
+    a.matched[cell] = m ? 1 : 0;
+  }
+  atomicAdd(a.evals + pair, (unsigned long long)(res.nvalid + a.extra_evals));
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D view of a plane buffer: x = column, y = row, z = plane index over all frames.
+static int encode_map(CUtensorMap* m, const void* base, const bmc_fme_params& p, int n_frames, int box_w, int box_h,
+                      int box_z) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BMC_E_CUDA;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)p.pad_w, (cuuint64_t)p.pad_h, (cuuint64_t)p.planes * n_frames};
+  const cuuint64_t strides[2] = {(cuuint64_t)p.pitch * p.elem_bytes, (cuuint64_t)p.plane_stride * p.elem_bytes};
+  const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, (cuuint32_t)box_z};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, p.elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) for box %dx%dx%d", (int)r, box_w, box_h, box_z);
+    return BMC_E_CUDA;
+  }
+  return BMC_OK;
+}
+
 static int pick_ty(int G) {
   const int groups = (G + 11) / 12;
   return (G + groups - 1) / groups;
 }
 
-static int geom_ref_words(int epw, int b, int r, int s) {
-  const int G = 2 * r + 1;
-  int gs = s % epw == 0 ? epw : (s % 2 == 0 ? 2 : 1);
-  if (gs > epw) gs = epw;
-  const int ncopies = G == 1 ? 1 : epw / gs;
-  const int wwin = 2 * r * s + b;
-  const int row_words = (wwin + epw - 1) / epw;
-  int cs = wwin * row_words;
-  cs += ((8 - (cs & 31)) + 32) & 31;
-  return ncopies * cs;
-}
-
 static const int kSmemBudget = 220 * 1024;
 static const int kSmemTarget = 110 * 1024;
 
-// Plan staging for stages (r[i], s[i]) of block size b.
-static int make_plan(SearchPlan& pl, const bmc_fme_params& p, int b, const int* rs, const int* ss, int nst) {
-  const int epw = 4 / p.elem_bytes;
-  pl.nmax = 1;
-  int refw = 0;
-  for (int i = 0; i < 3; ++i) pl.ty[i] = 1;
-  for (int i = 0; i < nst; ++i) {
-    const int G = 2 * rs[i] + 1;
-    pl.nmax = G * G > pl.nmax ? G * G : pl.nmax;
-    pl.ty[i] = pick_ty(G);
-    const int w = geom_ref_words(epw, b, rs[i], ss[i]);
-    refw = w > refw ? w : refw;
-  }
-  pl.ref_words = (refw + 3) & ~3;
-  pl.cur_words = b * b / epw;
-  const int fixed = 256 * 8 + kWarps * 20 + 16 * 4 + 4 * 8 + 16 + 2 * ((pl.nmax * 4 + 15) & ~15);
+int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma) {
+  std::memset(&pl, 0, sizeof pl);
+  const int eb = p.elem_bytes, epw = 4 / eb;
+  const int G = 2 * r + 1;
+  pl.ty = pick_ty(G);
+  pl.nmax = G * G;
+  const int wwin = 2 * r * s + b;
+  const int align = 16 / eb;  // TMA: inner box extent and start coordinate on 16-byte boundaries
+  static const bool no_tma = [] {
+    const char* e = getenv("BMC_NO_TMA");
+    return e && *e && *e != '0';
+  }();
+  // TMA box: the window widened by up to align-1 leading elements (16-byte aligned start) + 1 word of slack
+  const int bw_tma = (wwin + (align - 1) + epw + align - 1) / align * align;
+  pl.use_tma = (allow_tma && !no_tma && bw_tma <= 256 && wwin <= 256) ? 1 : 0;
+  pl.bw = pl.use_tma ? bw_tma : (wwin + epw + align - 1) / align * align;
+  pl.hwin = wwin;
+  pl.cbw = pl.use_tma ? (b * eb >= 16 ? b : align) : b;
+  pl.shift = pl.use_tma ? 1 : ((G > 1 && s % epw != 0) ? 1 : 0);
+  const int head = 256 * 8 + kWarps * 20 + 16 * 4 + 4 * 8 + 16;
+  pl.off_sad = (head + 127) & ~127;
+  pl.off_klist = pl.off_sad + ((pl.nmax * 4 + 127) & ~127);
+  pl.off_cur = pl.off_klist + ((pl.nmax * 4 + 127) & ~127);
   pl.pg = 0;
   for (int pg = p.planes; pg >= 1; --pg) {
-    const int total = fixed + pg * (pl.cur_words + pl.ref_words) * 4;
+    const int cur_bytes = pg * b * pl.cbw * eb;
+    const int win_bytes = pg * pl.hwin * pl.bw * eb;
+    const int off_win = pl.off_cur + ((cur_bytes + 127) & ~127);
+    const int total = off_win + win_bytes;
     if (total <= kSmemTarget || (pg == 1 && total <= kSmemBudget)) {
       pl.pg = pg;
+      pl.cur_bytes = cur_bytes;
+      pl.win_bytes = win_bytes;
+      pl.off_win = off_win;
       pl.smem = total;
       break;
     }
   }
   if (!pl.pg) {
-    set_error("search window of block %d with range/step (%d,%d) exceeds the %d KB shared-memory budget", b,
-              rs[0], ss[0], kSmemBudget / 1024);
+    set_error("search window of block %d with range %d step %d exceeds the %d KB shared-memory budget", b, r, s,
+              kSmemBudget / 1024);
     return BMC_E_SMEM;
   }
   return BMC_OK;
 }
 
-int launch_fme_level(const LevelArgs& a, int n_pairs, cudaStream_t st) {
-  const int epw = 4 / a.prm.elem_bytes;
-  const int cw = (a.b / epw) >= 4 ? 4 : 2;
-  dim3 grid(a.gw * a.gh, n_pairs);
-  cudaError_t e;
-#define BMC_LAUNCH_LEVEL(E, C)                                                                      \
-  do {                                                                                              \
-    e = cudaFuncSetAttribute(fme_level_kernel<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             a.plan.smem);                                                          \
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(fme_level)");                \
-    fme_level_kernel<E, C><<<grid, kThreads, a.plan.smem, st>>>(a);                                 \
-  } while (0)
-  if (a.prm.elem_bytes == 1) {
-    if (cw == 4) BMC_LAUNCH_LEVEL(uint8_t, 4); else BMC_LAUNCH_LEVEL(uint8_t, 2);
-  } else {
-    BMC_LAUNCH_LEVEL(uint16_t, 4);
+template <typename K>
+static int set_smem(K kern, int bytes) {
+  // cudaFuncSetAttribute is cheap but not free (and best kept out of graph
+  // capture): remember the largest value set per instantiation.
+  static std::mutex mu;
+  static const void* keys[512];
+  static int vals[512];
+  static int n = 0;
+  std::lock_guard<std::mutex> g(mu);
+  const void* key = reinterpret_cast<const void*>(kern);
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == key) {
+      if (vals[i] >= bytes) return BMC_OK;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+      vals[i] = bytes;
+      return BMC_OK;
+    }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+  if (n < 512) {
+    keys[n] = key;
+    vals[n] = bytes;
+    ++n;
   }
-#undef BMC_LAUNCH_LEVEL
-  return cuda_status(cudaGetLastError(), "fme_level_kernel");
+  return BMC_OK;
 }
 
-int plan_level(SearchPlan& pl, const bmc_fme_params& p, int b) {
-  return make_plan(pl, p, b, p.stage_range, p.stage_step, 3);
+static bool sync_debug() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BMC_SYNC_DEBUG");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v == 1;
 }
 
-int launch_stage(const StageArgs& a0, cudaStream_t st) {
-  StageArgs a = a0;
-  const int rs[1] = {a.r}, ss[1] = {a.s};
-  int rc = make_plan(a.plan, a.prm, a.b, rs, ss, 1);
+template <typename E, int CW, int TY, bool SH>
+static int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid, cudaStream_t st) {
+  int rc = set_smem(fme_stage_kernel<E, CW, TY, SH>, a.plan.smem);
   if (rc) return rc;
-  const int epw = 4 / a.prm.elem_bytes;
-  const int cw = (a.b / epw) >= 4 ? 4 : 2;
-  cudaError_t e;
-#define BMC_LAUNCH_STAGE(E, C)                                                                              \
-  do {                                                                                                      \
-    e = cudaFuncSetAttribute(stage_kernel<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.plan.smem); \
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(stage)");                            \
-    stage_kernel<E, C><<<1, kThreads, a.plan.smem, st>>>(a);                                                \
-  } while (0)
-  if (a.prm.elem_bytes == 1) {
-    if (cw == 4) BMC_LAUNCH_STAGE(uint8_t, 4); else BMC_LAUNCH_STAGE(uint8_t, 2);
-  } else {
-    BMC_LAUNCH_STAGE(uint16_t, 4);
+  fme_stage_kernel<E, CW, TY, SH><<<grid, kThreads, a.plan.smem, st>>>(tw, tc, a);
+  rc = cuda_status(cudaGetLastError(), "fme_stage_kernel");
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!rc && sync_debug() && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error("fme_stage_kernel<eb=%d,CW=%d,TY=%d,shift=%d> level %d b %d r %d s %d tma %d box %dx%dx%d cbw %d "
+                "smem %d: %s", (int)sizeof(E), CW, TY, (int)SH, a.level, a.b, a.r, a.s, a.plan.use_tma, a.plan.bw,
+                a.plan.hwin, a.plan.pg, a.plan.cbw, a.plan.smem, cudaGetErrorString(e));
+      return BMC_E_CUDA;
+    }
   }
-#undef BMC_LAUNCH_STAGE
-  return cuda_status(cudaGetLastError(), "stage_kernel");
+  return rc;
+}
+
+template <typename E, int CW, bool SH>
+static int dispatch_ty(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid,
+                       cudaStream_t st) {
+  switch (a.plan.ty) {
+    case 1: return launch_one<E, CW, 1, SH>(tw, tc, a, grid, st);
+    case 2: return launch_one<E, CW, 2, SH>(tw, tc, a, grid, st);
+    case 3: return launch_one<E, CW, 3, SH>(tw, tc, a, grid, st);
+    case 4: return launch_one<E, CW, 4, SH>(tw, tc, a, grid, st);
+    case 5: return launch_one<E, CW, 5, SH>(tw, tc, a, grid, st);
+    case 6: return launch_one<E, CW, 6, SH>(tw, tc, a, grid, st);
+    case 7: return launch_one<E, CW, 7, SH>(tw, tc, a, grid, st);
+    case 8: return launch_one<E, CW, 8, SH>(tw, tc, a, grid, st);
+    case 9: return launch_one<E, CW, 9, SH>(tw, tc, a, grid, st);
+    case 10: return launch_one<E, CW, 10, SH>(tw, tc, a, grid, st);
+    case 11: return launch_one<E, CW, 11, SH>(tw, tc, a, grid, st);
+    default: return launch_one<E, CW, 12, SH>(tw, tc, a, grid, st);
+  }
+}
+
+// Launch one stage.  The TMA maps view a.ref_planes (n_ref_frames frames) for
+// the window and a.planes (n_cur_frames) for the current block.
+int launch_fme_stage(const StageLaunch& a, int n_cur_frames, int n_ref_frames, dim3 grid, cudaStream_t st) {
+  CUtensorMap tw, tc;
+  std::memset(&tw, 0, sizeof tw);
+  std::memset(&tc, 0, sizeof tc);
+  if (a.plan.use_tma) {
+    int rc = encode_map(&tw, a.ref_planes, a.prm, n_ref_frames, a.plan.bw, a.plan.hwin, a.plan.pg);
+    if (rc) return rc;
+    rc = encode_map(&tc, a.planes, a.prm, n_cur_frames, a.plan.cbw, a.b, a.plan.pg);
+    if (rc) return rc;
+  }
+  const int epw = 4 / a.prm.elem_bytes;
+  const bool cw4 = (a.b / epw) >= 4;
+  const bool sh = a.plan.shift != 0;
+  if (a.prm.elem_bytes == 1) {
+    if (cw4)
+      return sh ? dispatch_ty<uint8_t, 4, true>(tw, tc, a, grid, st) : dispatch_ty<uint8_t, 4, false>(tw, tc, a, grid, st);
+    return sh ? dispatch_ty<uint8_t, 2, true>(tw, tc, a, grid, st) : dispatch_ty<uint8_t, 2, false>(tw, tc, a, grid, st);
+  }
+  return sh ? dispatch_ty<uint16_t, 4, true>(tw, tc, a, grid, st) : dispatch_ty<uint16_t, 4, false>(tw, tc, a, grid, st);
 }
 
 }  // namespace bmc

@@ -6,21 +6,32 @@
 
 namespace bmc {
 
-struct SearchPlan {
-  int ty[3];
-  int pg;
-  int nmax;
-  int ref_words;
-  int cur_words;
+// Host-computed plan of one search-stage launch (shared-memory layout, TMA boxes).
+struct StagePlan {
+  int ty;         // candidate rows per thread (template parameter TY)
+  int shift;      // sub-word candidate offsets need a funnel shift
+  int nmax;       // candidates (2r+1)^2
+  int pg;         // planes staged per pass
+  int bw;         // window box width (elements; 16-byte multiple, +1 word slack)
+  int hwin;       // window rows
+  int cbw;        // current-block box width (elements)
+  int use_tma;    // 1: TMA boxes, 0: plain-load staging (window too large for a box)
+  int cur_bytes, win_bytes;
+  int off_sad, off_klist, off_cur, off_win;
   int smem;
 };
-struct LevelArgs {
-  const void* planes;
+
+struct StageLaunch {
+  const void* planes;       // current-frame plane buffer
+  const void* ref_planes;   // reference-frame plane buffer (== planes for clips)
   bmc_fme_params prm;
-  SearchPlan plan;
+  StagePlan plan;
   const int32_t* cur_index;
   const int32_t* ref_index;
   int level, final_level, b, gw, gh;
+  int first, last;          // first / last searched stage of the level
+  int r, s;
+  int extra_evals;          // range-0 stages folded into this launch's candidate count
   const int32_t* parent_mv;
   const double* parent_e;
   const uint8_t* parent_matched;
@@ -29,18 +40,11 @@ struct LevelArgs {
   uint8_t* matched;
   unsigned long long* evals;
   const double* tab16;
+  int single;               // search_stage API: one block at (ox, oy), centre (cx, cy)
+  int ox, oy, cx, cy;
+  int32_t* nvalid_out;
 };
-struct StageArgs {
-  const void* cur;
-  const void* ref;
-  bmc_fme_params prm;
-  SearchPlan plan;
-  int ox, oy, b, cx, cy, r, s;
-  int32_t* mv;
-  double* energy;
-  int32_t* nvalid;
-  const double* tab16;
-};
+
 struct RefineArgs {
   const int32_t* mv_in;
   const double* e_in;
@@ -85,9 +89,8 @@ struct PredictArgs {
   int gh, gw, B, scale;
 };
 
-int plan_level(SearchPlan& pl, const bmc_fme_params& p, int b);
-int launch_fme_level(const LevelArgs& a, int n_pairs, cudaStream_t st);
-int launch_stage(const StageArgs& a, cudaStream_t st);
+int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma);
+int launch_fme_stage(const StageLaunch& a, int n_cur_frames, int n_ref_frames, dim3 grid, cudaStream_t st);
 int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p, void* planes, cudaStream_t st);
 int launch_refine(const RefineArgs& a, cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);

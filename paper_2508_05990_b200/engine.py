@@ -144,7 +144,7 @@ class ClipEngine:
             return
         if self.cfg.reference_policy == "previous":
             arr = self._level_slice(0, self.n_pairs)
-            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), ctypes.byref(p), self.n_pairs,
+            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), self.S * self.T, ctypes.byref(p), self.n_pairs,
                                             N.ptr(self.cur_index), N.ptr(self.ref_index), arr, st))
             self._refine(0, self.n_pairs)
             self._decide(1, self.T)
@@ -153,7 +153,7 @@ class ClipEngine:
         for t in range(1, self.T):
             lo, hi = (t - 1) * S, t * S
             arr = self._level_slice(lo, hi)
-            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), ctypes.byref(p), S, N.ptr(self.cur_index[lo:hi]),
+            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), self.S * self.T, ctypes.byref(p), S, N.ptr(self.cur_index[lo:hi]),
                                             N.ptr(self.ref_index[lo:hi]), arr, st))
             self._refine(lo, hi)
             nxt = N.ptr(self.ref_index[hi:hi + S]) if t + 1 < self.T else None

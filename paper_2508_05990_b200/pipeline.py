@@ -115,12 +115,13 @@ def run_sequence(frames, key_labels, config: PipelineConfig = PipelineConfig(), 
     labels, decisions = [], []
     fin = eng.levels[-1]
     evals = [lv.evals[:eng.n_pairs].cpu().numpy() for lv in eng.levels]
-    replaced = eng.replaced[:eng.n_pairs].cpu().numpy()
+    # count_replacements (mv_refine.py:72-73) counts changed vectors
+    changed = (fin.mv[:eng.n_pairs] != eng.mv_ref[:eng.n_pairs]).any(dim=-1).sum(dim=(1, 2)).cpu().numpy()
     for i, f in enumerate(frames):
         if i > 0:
             p = eng.pair_index(0, i)
             ledger.add("fme", count_fme_flops((f.width, f.height), config.fme, [int(e[p]) for e in evals], planes))
-            ledger.add("mv_refine", count_refine_flops(fin.gw, fin.gh, eng.b_final, int(replaced[p].sum()), planes))
+            ledger.add("mv_refine", count_refine_flops(fin.gw, fin.gh, eng.b_final, int(changed[p]), planes))
         if kinds[i] == 0:
             ledger.add("backbone", backbone)
             lab = injected[i]
@@ -132,3 +133,62 @@ def run_sequence(frames, key_labels, config: PipelineConfig = PipelineConfig(), 
             decisions.append(FrameDecision(i, kind_from_code(kinds[i]), ref, float(trig[i])))
         labels.append(lab)
     return RunResult(labels=labels, decisions=decisions, ledger=ledger, scale=scale)
+
+
+class ClipSession:
+    """Reusable host-buffer clip API (the batched public entry point).
+
+    ``run(raw, key_labels)`` takes a (T, H, W) uint8/uint16 Bayer (or luma)
+    clip in host memory, runs ME -> refine -> decide -> predict on the GPU and
+    returns ``(labels (T, Hl, Wl) uint8 ndarray, kinds, refs, triggers)``.
+    ``key_labels`` is a callable / mapping frame -> LabelMap consulted exactly
+    once per key frame, as in ``run_sequence``.  Device buffers and pinned
+    staging buffers are allocated once per session, so repeated clips of the
+    same geometry pay only the transfers and the kernels.
+    """
+
+    def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
+                 bayer: bool = True):
+        if config.refine_enabled:
+            raise NotImplementedError("CaBR-Net block refinement is not part of the B200 hot path yet; "
+                                      "run with PipelineConfig(refine_enabled=False)")
+        self.eng = ClipEngine(config, height, width, n_frames, 1, dtype, bayer)
+        torch = self.eng.torch
+        self.torch = torch
+        self.pin_raw = torch.empty(tuple(self.eng.raw.shape[1:]), dtype=self.eng.raw.dtype).pin_memory()
+        self.pin_labels = torch.empty(tuple(self.eng.labels.shape[1:]), dtype=torch.uint8).pin_memory()
+        self.pin_key = torch.empty(tuple(self.eng.labels.shape[1:]), dtype=torch.uint8).pin_memory()
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def run(self, raw, key_labels):
+        eng, torch = self.eng, self.torch
+        lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
+        src = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(raw))
+        if src.is_pinned():
+            eng.raw[0].copy_(src, non_blocking=True)
+        else:
+            self.pin_raw.copy_(src)
+            eng.raw[0].copy_(self.pin_raw, non_blocking=True)
+        h2d = src.numel() * src.element_size()
+        eng.motion()
+        kinds, refs, trig = (a[0] for a in eng.decisions_host())
+        d2h = kinds.nbytes + refs.nbytes + trig.nbytes
+        for i in np.nonzero(kinds == 0)[0].tolist():
+            try:
+                lab = lookup(i)
+            except (KeyError, IndexError, FileNotFoundError):
+                raise MissingKeyLabels(i) from None
+            if lab is None:
+                raise MissingKeyLabels(i)
+            if (lab.height, lab.width) != (eng.Hl, eng.Wl):
+                raise ValueError("key label maps must match the session's label size")
+            self.pin_key[i].copy_(torch.from_numpy(np.array(lab.classes)))
+            eng.key_labels[0, i].copy_(self.pin_key[i], non_blocking=True)
+            h2d += lab.classes.nbytes
+        eng.predict()
+        self.pin_labels.copy_(eng.labels[0], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        d2h += self.pin_labels.numel()
+        self.h2d_bytes, self.d2h_bytes = h2d, d2h
+        return self.pin_labels.numpy(), kinds, refs, trig
