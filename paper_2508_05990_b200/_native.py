@@ -13,7 +13,10 @@ import math
 import threading
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libbmc_b200.so"
+import os
+
+# BMC_LIB_PATH lets kernel-variant experiments (tools/) point at another build.
+_LIB_PATH = Path(os.environ.get("BMC_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libbmc_b200.so")
 
 BMC_OK, BMC_E_ARG, BMC_E_CUDA, BMC_E_NOVALID, BMC_E_SMEM = 0, 1, 2, 3, 4
 KIND_LUMA, KIND_BAYER = 0, 1
@@ -87,7 +90,7 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing:
+        if build_if_missing and "BMC_LIB_PATH" not in os.environ:
             from . import build as _build
             try:
                 _build.build()

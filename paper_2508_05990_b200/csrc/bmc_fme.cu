@@ -44,14 +44,23 @@ namespace bmc {
 
 constexpr double kScreenEps = 1e-11;
 
+#ifndef BMC_SEARCH_THREADS
+#define BMC_SEARCH_THREADS 128
+#endif
+#ifndef BMC_SEARCH_MINB
+#define BMC_SEARCH_MINB 4
+#endif
+constexpr int kST = BMC_SEARCH_THREADS;  // threads per search CTA
+constexpr int kSW = kST / 32;            // warps per search CTA
+
 // ---------------------------------------------------------------------------
 // shared-memory carve-up
 // ---------------------------------------------------------------------------
 struct SmemLayout {
   double* tab;                 // fl(v/255) for uint8
-  unsigned long long* red64;   // [kWarps]
-  double* best_e;              // [kWarps]
-  int* best_k;                 // [kWarps]
+  unsigned long long* red64;   // [kSW]
+  double* best_e;              // [kSW]
+  int* best_k;                 // [kSW]
   int* misc;                   // [16]
   double* miscd;               // [4]
   unsigned long long* bar;     // mbarrier
@@ -66,11 +75,11 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   L.tab = reinterpret_cast<double*>(base);
   unsigned char* p = base + 256 * sizeof(double);
   L.red64 = reinterpret_cast<unsigned long long*>(p);
-  p += kWarps * 8;
+  p += kSW * 8;
   L.best_e = reinterpret_cast<double*>(p);
-  p += kWarps * 8;
+  p += kSW * 8;
   L.best_k = reinterpret_cast<int*>(p);
-  p += kWarps * 4;
+  p += kSW * 4;
   L.misc = reinterpret_cast<int*>(p);
   p += 16 * 4;
   L.miscd = reinterpret_cast<double*>(p);
@@ -158,7 +167,7 @@ __device__ void stage_ldg(const SmemLayout& L, const Elem* __restrict__ cur0, co
   const int bww = pl.bw / EPW;
   const int row_max_w = pitch / EPW - 1;
   const int total = npl * pl.hwin * bww;
-  for (int idx = threadIdx.x; idx < total; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < total; idx += kST) {
     const int w = idx % bww;
     const int row = (idx / bww) % pl.hwin;
     const int pp = idx / (bww * pl.hwin);
@@ -170,11 +179,11 @@ __device__ void stage_ldg(const SmemLayout& L, const Elem* __restrict__ cur0, co
         reinterpret_cast<const uint32_t*>(ref0 + (long long)pp * plane_stride + (long long)gy * pitch);
     const uint32_t lo = __ldg(row32 + min(max(gw0, 0), row_max_w));
     const uint32_t v = sh ? __funnelshift_r(lo, __ldg(row32 + min(max(gw0 + 1, 0), row_max_w)), sh * SH) : lo;
-    L.win[(pp * pl.hwin + row) * bww + w] = v;
+    L.win[(pp * pl.wrows + row) * bww + w] = v;
   }
   const int cbw = pl.cbw / EPW, cw = b / EPW;
   const int ctot = npl * b * cw;
-  for (int idx = threadIdx.x; idx < ctot; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < ctot; idx += kST) {
     const int w = idx % cw;
     const int row = (idx / cw) % b;
     const int pp = idx / (cw * b);
@@ -217,59 +226,88 @@ __device__ __forceinline__ void load_row(uint32_t (&dst)[CW], const uint32_t* sr
 
 // Phase A: integer SAD of every (candidate column, TY-row group, chunk, staged
 // plane) item; partial sums meet in L.sad via shared atomics.
+// Phase A: integer SAD.  Work item = (candidate column i, TY-row group gi,
+// part) where `part` is one of pl.parts contiguous slices of the (plane,
+// chunk) units of the block.  With one part a thread owns its TY candidates
+// completely and stores the sums; otherwise partial sums meet via shared
+// atomics.  The host picks the part count that best fills the CTA.
 template <typename Elem, int CW, int TY, bool SHIFT>
 __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int npl, const StagePlan& pl,
-                          int coff_w) {
+                          int coff_w, bool accumulate) {
   constexpr int EPW = 4 / sizeof(Elem);
   const int bww = pl.bw / EPW;
   const int cbw = pl.cbw / EPW;
   const int cpr = (b / EPW) / CW;
-  const int items = g.G * g.ncg * cpr * npl;
+  const int units = npl * cpr;
+  const int parts = min(pl.parts, units);
+  const int per = (units + parts - 1) / parts;
+  const int cols = g.G * g.ncg;
+  const int items = cols * parts;
   const int s = g.s;
   const int nrho = s < b ? s : b;
-  const int hmax = pl.hwin - 1;
-  for (int it = threadIdx.x; it < items; it += kThreads) {
-    int t = it;
-    const int i = t % g.G;
-    t /= g.G;
-    const int gi = t % g.ncg;
-    t /= g.ncg;
-    const int c = t % cpr;
-    const int pp = t / cpr;
+  const int rstep = s * bww, cstep = s * cbw;
+  // incremental mixed-radix decode of it = (part * ncg + gi) * G + i
+  int i = threadIdx.x % g.G, q = threadIdx.x / g.G;
+  const int di = kST % g.G, dq = kST / g.G;
+  for (int it = threadIdx.x; it < items; it += kST) {
+    const int gi = q % g.ncg, part = q / g.ncg;
     const int xo = g.d + i * s;
     const int sh = (xo % EPW) * 8 * (int)sizeof(Elem);
-    const uint32_t* R0 = L.win + pp * pl.hwin * bww + (xo / EPW) + c * CW;
-    const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + c * CW;
     uint32_t acc[TY];
 #pragma unroll
     for (int j = 0; j < TY; ++j) acc[j] = 0;
-    for (int rho = 0; rho < nrho; ++rho) {
-      const int M = (b - 1 - rho) / s + 1;
-      const int base = rho + gi * TY * s;
-      uint32_t R[TY][CW];
+    const int u_end = min(units, (part + 1) * per);
+    for (int u = part * per; u < u_end; ++u) {
+      const int pp = u / cpr, c = u - pp * cpr;
+      // window rows past hwin (next plane / slack rows) only feed the padding
+      // candidates of the last row group, whose sums are discarded.
+      const uint32_t* R0 = L.win + pp * pl.wrows * bww + (xo / EPW) + c * CW;
+      const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + c * CW;
+      for (int rho = 0; rho < nrho; ++rho) {
+        const int M = (b - 1 - rho) / s + 1;
+        const uint32_t* rp = R0 + (rho + gi * TY * s) * bww;
+        const uint32_t* cp = C0 + rho * cbw;
+        uint32_t R[TY][CW];
 #pragma unroll
-      for (int k = 0; k < TY - 1; ++k) load_row<CW, SHIFT>(R[k], R0 + min(base + k * s, hmax) * bww, sh);
-      for (int m0 = 0; m0 < M; m0 += TY) {
+        for (int k = 0; k < TY - 1; ++k) load_row<CW, SHIFT>(R[k], rp + k * rstep, sh);
+        rp += (TY - 1) * rstep;
+        for (int m0 = 0; m0 < M; m0 += TY) {
 #pragma unroll
-        for (int k = 0; k < TY; ++k) {
-          const int m = m0 + k;
-          if (m < M) {
-            load_row<CW, SHIFT>(R[(k + TY - 1) % TY], R0 + min(base + (m + TY - 1) * s, hmax) * bww, sh);
-            uint32_t C[CW];
-            load_cur<CW>(C, C0 + (rho + m * s) * cbw);
+          for (int k = 0; k < TY; ++k) {
+            if (m0 + k < M) {
+              load_row<CW, SHIFT>(R[(k + TY - 1) % TY], rp, sh);
+              rp += rstep;
+              uint32_t C[CW];
+              load_cur<CW>(C, cp);
+              cp += cstep;
 #pragma unroll
-            for (int j = 0; j < TY; ++j) {
+              for (int j = 0; j < TY; ++j) {
 #pragma unroll
-              for (int w = 0; w < CW; ++w) acc[j] = sad_word(C[w], R[(k + j) % TY][w], acc[j], Elem());
+                for (int w = 0; w < CW; ++w) acc[j] = sad_word(C[w], R[(k + j) % TY][w], acc[j], Elem());
+              }
             }
           }
         }
       }
     }
+    if (!accumulate) {
 #pragma unroll
-    for (int j = 0; j < TY; ++j) {
-      const int jj = gi * TY + j;
-      if (jj < g.G) atomicAdd(&L.sad[jj * g.G + i], acc[j]);
+      for (int j = 0; j < TY; ++j) {
+        const int jj = gi * TY + j;
+        if (jj < g.G) L.sad[jj * g.G + i] = acc[j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TY; ++j) {
+        const int jj = gi * TY + j;
+        if (jj < g.G) atomicAdd(&L.sad[jj * g.G + i], acc[j]);
+      }
+    }
+    i += di;
+    q += dq;
+    if (i >= g.G) {
+      i -= g.G;
+      ++q;
     }
   }
 }
@@ -288,12 +326,23 @@ __device__ __forceinline__ bool cand_valid_ij(const StageGeom& g, int ox, int oy
   return x >= 0 && x <= fw - b && y >= 0 && y <= fh - b;
 }
 
+// Exact energy of candidate (i, j).  When every plane is resident in shared
+// memory (pg == P) the replay reads the staged tiles; otherwise global memory.
 template <typename Elem>
-__device__ __forceinline__ double exact_cand(const PairCtx<Elem>& pc, int ox, int oy, int b, int dx, int dy) {
+__device__ __forceinline__ double exact_cand(const SmemLayout& L, const StagePlan& pl, const StageGeom& g,
+                                             const PairCtx<Elem>& pc, int ox, int oy, int b, int coff, int i, int j,
+                                             int dx, int dy) {
+  if (pl.pg == pc.P) {
+    const Elem* cur = reinterpret_cast<const Elem*>(L.cur) + coff;
+    const Elem* ref = reinterpret_cast<const Elem*>(L.win) + (long long)(j * g.s) * pl.bw + g.d + i * g.s;
+    return exact_energy_generic<Elem>(cur, pl.cbw, (long long)b * pl.cbw, ref, pl.bw, (long long)pl.wrows * pl.bw, b,
+                                      pc.P, pc.tab, pc.tol, pc.oml, pc.lam)
+        .energy;
+  }
   const long long roff = (long long)(oy + dy) * pc.pitch + (ox + dx);
-  const long long coff = (long long)oy * pc.pitch + ox;
-  return exact_energy_warp<Elem>(pc.cur + coff, pc.ref + roff, pc.pitch, pc.plane_stride, b, pc.P, pc.tab, pc.tol,
-                                 pc.oml, pc.lam)
+  const long long coffg = (long long)oy * pc.pitch + ox;
+  return exact_energy_generic<Elem>(pc.cur + coffg, pc.pitch, pc.plane_stride, pc.ref + roff, pc.pitch,
+                                    pc.plane_stride, b, pc.P, pc.tab, pc.tol, pc.oml, pc.lam)
       .energy;
 }
 
@@ -317,18 +366,21 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   g.d = g.wx0 - g.tx0;
   const int cx0 = pl.use_tma ? ox - (ox % A16) : ox;  // ox >= 0
   const int coff_w = (ox - cx0) / (4 / (int)sizeof(Elem));
+  const int coff_e = ox - cx0;  // element offset of the block inside each staged cur row
   const int N = g.G * g.G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = pc.P * b * b;
 
   __syncthreads();  // previous users of smem are done; mbarrier init visible
-  for (int k = tid; k < N; k += kThreads) L.sad[k] = 0;
+  const bool accumulate = pl.parts > 1 || pl.pg < pc.P;
+  if (accumulate)
+    for (int k = tid; k < N; k += kST) L.sad[k] = 0;
   for (int p0 = 0; p0 < pc.P; p0 += pl.pg) {
     const int npl = min(pl.pg, pc.P - p0);
     if (p0) __syncthreads();
     if (pl.use_tma) {
       if (tid == 0) {
-        mbar_expect_tx(L.bar, (uint32_t)(pl.win_bytes + pl.cur_bytes));  // full boxes, OOB included
+        mbar_expect_tx(L.bar, (uint32_t)(pl.tma_bytes));  // full boxes, OOB included
         tma_load_3d(L.win, tm_win, g.tx0, g.wy0, pc.ref_z + p0, L.bar);
         tma_load_3d(L.cur, tm_cur, cx0, oy, pc.cur_z + p0, L.bar);
       }
@@ -339,7 +391,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
                       pc.plane_stride, pc.frame_h, g, ox, oy, b, npl, pl);
     }
     __syncthreads();
-    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w);
+    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, accumulate);
   }
   __syncthreads();
 
@@ -348,8 +400,8 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   int nvalid = 0;
   {
     int i = tid % g.G, j = tid / g.G;
-    const int di = kThreads % g.G, dj = kThreads / g.G;
-    for (int k = tid; k < N; k += kThreads) {
+    const int di = kST % g.G, dj = kST / g.G;
+    for (int k = tid; k < N; k += kST) {
       int dx, dy;
       if (cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, i, j, dx, dy)) {
         ++nvalid;
@@ -377,7 +429,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   if (tid == 0) {
     unsigned long long b0 = L.red64[0];
     int nv = L.best_k[0];
-    for (int w = 1; w < kWarps; ++w) {
+    for (int w = 1; w < kSW; ++w) {
       b0 = L.red64[w] < b0 ? L.red64[w] : b0;
       nv += L.best_k[w];
     }
@@ -403,12 +455,15 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
     res.energy = 0.0;
     return res;
   }
+  if (sizeof(Elem) == 1)  // fl(v/255) table for the exact replays (only blocks that reach here pay for it)
+    for (int v = tid; v < 256; v += kST) L.tab[v] = __ddiv_rn((double)v, (double)pc.max_value);
+  __syncthreads();
   if (warp == 0) {
     double e0 = 0.0;
     if (sad0 != 0) {
       int dx, dy;
       cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, dx, dy);
-      e0 = exact_cand<Elem>(pc, ox, oy, b, dx, dy);
+      e0 = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, m0 % g.G, m0 / g.G, dx, dy);
     }
     if (lane == 0) L.miscd[0] = e0;
   }
@@ -418,8 +473,8 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   const double unit = (double)pc.max_value * (double)n;
   {
     int i = tid % g.G, j = tid / g.G;
-    const int di = kThreads % g.G, dj = kThreads / g.G;
-    for (int k = tid; k < N; k += kThreads) {
+    const int di = kST % g.G, dj = kST / g.G;
+    for (int k = tid; k < N; k += kST) {
       int dx, dy;
       if (k != m0 && cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, i, j, dx, dy)) {
         const double lb = pc.oml * ((double)L.sad[k] / unit);
@@ -437,11 +492,11 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   const int nk = L.misc[3];
   double be = (warp == 0) ? e0 : 1e300;
   int bk = (warp == 0) ? m0 : 0x7fffffff;
-  for (int e = warp; e < nk; e += kWarps) {
+  for (int e = warp; e < nk; e += kSW) {
     const int k = L.klist[e];
     int dx, dy;
     cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, k % g.G, k / g.G, dx, dy);
-    const double ek = exact_cand<Elem>(pc, ox, oy, b, dx, dy);
+    const double ek = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, k % g.G, k / g.G, dx, dy);
     if (ek < be || (ek == be && k < bk)) {
       be = ek;
       bk = k;
@@ -455,7 +510,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   if (tid == 0) {
     double e = L.best_e[0];
     int k = L.best_k[0];
-    for (int w = 1; w < kWarps; ++w) {
+    for (int w = 1; w < kSW; ++w) {
       if (L.best_e[w] < e || (L.best_e[w] == e && L.best_k[w] < k)) {
         e = L.best_e[w];
         k = L.best_k[w];
@@ -475,7 +530,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
 // the stage kernel
 // ---------------------------------------------------------------------------
 template <typename Elem, int CW, int TY, bool SHIFT>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kST, BMC_SEARCH_MINB)
     fme_stage_kernel(const __grid_constant__ CUtensorMap tm_win, const __grid_constant__ CUtensorMap tm_cur,
                      const StageLaunch a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -535,12 +590,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   pc.tol = p.sparsity_tolerance;
   pc.lam = p.lam;
   pc.oml = p.one_minus_lam;
-  if (sizeof(Elem) == 1) {
-    for (int v = threadIdx.x; v < 256; v += kThreads) L.tab[v] = __ddiv_rn((double)v, (double)p.max_value);
-    pc.tab = L.tab;
-  } else {
-    pc.tab = a.tab16;
-  }
+  pc.tab = sizeof(Elem) == 1 ? L.tab : a.tab16;  // the uint8 table is filled lazily (first exact replay)
   uint32_t phase = 0;
   if (a.plan.use_tma && threadIdx.x == 0) mbar_init(L.bar, 1);
   StageResult res = stage_search<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox, oy, b, sx, sy, a.r,
@@ -612,7 +662,12 @@ static int encode_map(CUtensorMap* m, const void* base, const bmc_fme_params& p,
 }
 
 static int pick_ty(int G) {
-  const int groups = (G + 11) / 12;
+  static const int cap = [] {
+    const char* e = getenv("BMC_TY_MAX");
+    const int v = e ? atoi(e) : 12;
+    return v >= 1 && v <= 12 ? v : 12;
+  }();
+  const int groups = (G + cap - 1) / cap;
   return (G + groups - 1) / groups;
 }
 
@@ -636,24 +691,47 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
   pl.use_tma = (allow_tma && !no_tma && bw_tma <= 256 && wwin <= 256) ? 1 : 0;
   pl.bw = pl.use_tma ? bw_tma : (wwin + epw + align - 1) / align * align;
   pl.hwin = wwin;
+  {
+    // parts per (column, row-group): fill the CTA without splitting when the grid is large
+    const int cols = G * ((G + pl.ty - 1) / pl.ty);
+    const int units_max = p.planes * ((b / epw) / ((b / epw) >= 4 ? 4 : 2));
+    int best = 1;
+    double best_u = 0.0;
+    for (int parts = 1; parts <= units_max; ++parts) {
+      const int items = cols * parts;
+      const int rounds = (items + kST - 1) / kST;
+      const double util = (double)items / (rounds * kST) - 0.02 * (parts > 1);  // atomics cost a little
+      if (util > best_u + 1e-9) {
+        best_u = util;
+        best = parts;
+      }
+    }
+    pl.parts = best;
+  }
+  // plane stride in smem = hwin rows (the 3-D TMA box is written densely); the
+  // padding rows of the last row group run into the next plane (harmless: their
+  // sums are discarded) and past the last plane into ty*s slack rows.
+  pl.wrows = wwin;
   pl.cbw = pl.use_tma ? (b * eb >= 16 ? b : align) : b;
   pl.shift = pl.use_tma ? 1 : ((G > 1 && s % epw != 0) ? 1 : 0);
-  const int head = 256 * 8 + kWarps * 20 + 16 * 4 + 4 * 8 + 16;
+  const int head = 256 * 8 + kSW * 20 + 16 * 4 + 4 * 8 + 16;
   pl.off_sad = (head + 127) & ~127;
   pl.off_klist = pl.off_sad + ((pl.nmax * 4 + 127) & ~127);
   pl.off_cur = pl.off_klist + ((pl.nmax * 4 + 127) & ~127);
   pl.pg = 0;
   for (int pg = p.planes; pg >= 1; --pg) {
     const int cur_bytes = pg * b * pl.cbw * eb;
-    const int win_bytes = pg * pl.hwin * pl.bw * eb;
+    const int win_bytes = (pg * pl.wrows + pl.ty * s) * pl.bw * eb;
     const int off_win = pl.off_cur + ((cur_bytes + 127) & ~127);
     const int total = off_win + win_bytes;
     if (total <= kSmemTarget || (pg == 1 && total <= kSmemBudget)) {
       pl.pg = pg;
+      if (pg < p.planes && pl.parts < 2) pl.parts = 2;  // several staging passes accumulate -> atomics
       pl.cur_bytes = cur_bytes;
       pl.win_bytes = win_bytes;
       pl.off_win = off_win;
       pl.smem = total;
+      pl.tma_bytes = cur_bytes + pg * pl.hwin * pl.bw * eb;
       break;
     }
   }
@@ -706,7 +784,7 @@ template <typename E, int CW, int TY, bool SH>
 static int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid, cudaStream_t st) {
   int rc = set_smem(fme_stage_kernel<E, CW, TY, SH>, a.plan.smem);
   if (rc) return rc;
-  fme_stage_kernel<E, CW, TY, SH><<<grid, kThreads, a.plan.smem, st>>>(tw, tc, a);
+  fme_stage_kernel<E, CW, TY, SH><<<grid, kST, a.plan.smem, st>>>(tw, tc, a);
   rc = cuda_status(cudaGetLastError(), "fme_stage_kernel");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (!rc && sync_debug() && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {

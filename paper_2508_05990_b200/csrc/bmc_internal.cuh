@@ -83,12 +83,12 @@ struct ExactResult {
 // a+b == b+a bit for bit).  Remaining levels combine per-lane partials with a
 // binary-carry stack, which is the same perfect tree.
 //
-// cur/ref: plane-0 pointers of the block / candidate window (element units,
-// `pitch` per row, `plane_stride` per plane).
+// cur/ref: element (0,0) of plane 0 of the block / candidate window, with their
+// own row pitch and plane stride (global planes or staged shared-memory tiles).
 template <typename Elem>
-__device__ ExactResult exact_energy_warp(const Elem* __restrict__ cur, const Elem* __restrict__ ref,
-                                         int pitch, long long plane_stride, int b, int P,
-                                         const double* tab, double tol, double oml, double lam) {
+__device__ ExactResult exact_energy_generic(const Elem* cur, int cpitch, long long cplane, const Elem* ref, int rpitch,
+                                            long long rplane, int b, int P, const double* tab, double tol, double oml,
+                                            double lam) {
   const int lane = threadIdx.x & 31;
   const int lb = __ffs(b) - 1;
   const int n = P << (2 * lb);
@@ -109,8 +109,9 @@ __device__ ExactResult exact_energy_warp(const Elem* __restrict__ cur, const Ele
         const int p = e >> (2 * lb);
         const int y = (e >> lb) & (b - 1);
         const int x = e & (b - 1);
-        const long long off_c = p * plane_stride + (long long)y * pitch + x;
-        const double dv = fabs(__dsub_rn(norm_sample(ref[off_c], tab), norm_sample(cur[off_c], tab)));
+        const double cv = norm_sample(cur[p * cplane + (long long)y * cpitch + x], tab);
+        const double rv = norm_sample(ref[p * rplane + (long long)y * rpitch + x], tab);
+        const double dv = fabs(__dsub_rn(rv, cv));
         cnt += dv > tol;
         r = (t == 0) ? dv : __dadd_rn(r, dv);
       }
@@ -143,6 +144,14 @@ __device__ ExactResult exact_energy_warp(const Elem* __restrict__ cur, const Ele
   res.count = cnt;
   res.energy = __dadd_rn(__dmul_rn(oml, __ddiv_rn(s_f, nd)), __dmul_rn(lam, __ddiv_rn((double)cnt, nd)));
   return res;
+}
+
+// Global-memory form: both operands in the same plane layout.
+template <typename Elem>
+__device__ ExactResult exact_energy_warp(const Elem* __restrict__ cur, const Elem* __restrict__ ref, int pitch,
+                                         long long plane_stride, int b, int P, const double* tab, double tol,
+                                         double oml, double lam) {
+  return exact_energy_generic<Elem>(cur, pitch, plane_stride, ref, pitch, plane_stride, b, P, tab, tol, oml, lam);
 }
 
 // ---------------------------------------------------------------------------

@@ -9,14 +9,16 @@ namespace bmc {
 // Host-computed plan of one search-stage launch (shared-memory layout, TMA boxes).
 struct StagePlan {
   int ty;         // candidate rows per thread (template parameter TY)
+  int parts;      // (plane, chunk) slices per candidate column group (1 = no atomics)
   int shift;      // sub-word candidate offsets need a funnel shift
   int nmax;       // candidates (2r+1)^2
   int pg;         // planes staged per pass
   int bw;         // window box width (elements; 16-byte multiple, +1 word slack)
-  int hwin;       // window rows
+  int hwin;       // window rows (TMA box height)
+  int wrows;      // allocated window rows per plane (hwin + slack)
   int cbw;        // current-block box width (elements)
   int use_tma;    // 1: TMA boxes, 0: plain-load staging (window too large for a box)
-  int cur_bytes, win_bytes;
+  int cur_bytes, win_bytes, tma_bytes;
   int off_sad, off_klist, off_cur, off_win;
   int smem;
 };
