@@ -296,7 +296,10 @@ def run_b200(args, rank, world, local_rank):
     # parity spot check of the e2e result against the graph result
     e2e_ok = bool(np.array_equal(out_labels, eng.labels[0].cpu().numpy()))
 
-    # --- max over ranks ---
+    # --- max over ranks (the only collective: one tiny exchange after timing) ---
+    from paper_2508_05990_b200 import sharding
+    digest = sharding.parity_hash(eng.labels[0].cpu().numpy(), eng.kind.cpu().numpy())
+    stats = sharding.gather_stats((T - 1) * args.steps, total_ms / 1e3, digest, device=dev)
     vals = torch.tensor([total_ms, statistics.mean(e2e_ms), me_avg], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
@@ -348,6 +351,8 @@ def run_b200(args, rank, world, local_rank):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "keyframes_per_clip": int((eng.kind[0] == 0).sum().item()),
+        "ranks": [{"frames": int(r[0]), "seconds": float(r[1]),
+                   "parity_hash": f"{int(r[3]) << 32 | int(r[2]):016x}"} for r in stats],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
