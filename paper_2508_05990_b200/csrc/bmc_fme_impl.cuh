@@ -1,0 +1,867 @@
+// Block-matching motion estimation on packed Bayer / luma planes (sm_100a):
+// device code of the stage kernel (included by the bmc_fme_k_*.cu instantiation units).
+//
+// Replaces fme.estimate_motion / _search_block / _stage_candidates
+// (fme.py:236-392) and search_stage (fme.py:271-291).
+//
+// One launch per (level, search stage); one CTA per (frame pair, block).  The
+// three chained stages of a block (fme.py:306-315) communicate through the
+// level's mv/energy arrays; stages with range 0 after a searched stage select
+// the same candidate again and are folded into the candidate count on the
+// host (no launch).  Per stage:
+//
+//   staging  one TMA box (cp.async.bulk.tensor.3d) brings the reference window
+//            (candidate grid + block halo, all staged planes) into shared
+//            memory and a second box the current block; the tensor map's
+//            out-of-bounds zero fill covers frame borders (those windows only
+//            belong to invalid candidates).  TMA boxes must start on a 16-byte
+//            boundary, so candidates whose window starts inside a 32-bit word
+//            read one of up to three pre-shifted copies of the window, built
+//            once per stage (one funnel shift per staged word instead of one
+//            per loaded word per candidate row).
+//   A        integer screening.  A work item is (candidate column, TY-row
+//            group, part) where a part is a slice of the (plane, chunk) units
+//            of the block.  The item slides a TY-row register window down the
+//            block so every loaded reference word feeds TY packed SAD
+//            instructions (VABSDIFF4.U8.ACC for uint8; VIMNMX.U16x2 x2 +
+//            IDP.2A for uint16).  The window advances over exactly the block's
+//            rows (full TY-periods unrolled, then an unrolled tail with a
+//            uniform early exit), so no SAD instruction is issued predicated
+//            off.  Each part owns a partial-sum array (no atomics); the CTA size
+//            is chosen on the host so the items fill whole warps.
+//   B        exact selection.  E >= (1-lam)*SAD/(s*n) because the sparsity
+//            term is >= 0, so only candidates whose integer lower bound does
+//            not exceed the exact energy of the min-SAD candidate (+1e-11, far
+//            above the ~1e-15 float error) can win.  They are replayed in
+//            float64 in numpy's pairwise order (bmc_internal.cuh); the first
+//            minimum in canonical dy-major order wins (np.argmin, fme.py:266).
+//            A min SAD of 0 has E == 0 exactly and wins outright (lam < 1).
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "bmc_internal.cuh"
+#include "bmc_launch.cuh"
+
+namespace bmc {
+
+constexpr double kScreenEps = 1e-11;
+#ifndef BMC_STAGE_MINB
+#define BMC_STAGE_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+constexpr int kMaxSW = ((kMaxStageThreads + 31) / 32 + 1) / 2 * 2;  // warps per search CTA (max, even: keeps the
+                                                                 // 8-byte members of the smem head aligned)
+
+// ---------------------------------------------------------------------------
+// shared-memory carve-up
+// ---------------------------------------------------------------------------
+struct SmemLayout {
+  double* tab;                 // fl(v/255) for uint8
+  unsigned long long* red64;   // [kMaxSW]
+  double* best_e;              // [kMaxSW]
+  int* best_k;                 // [kMaxSW]
+  int* misc;                   // [16]
+  double* miscd;               // [4]
+  unsigned long long* bar;     // mbarrier
+  uint32_t* sad;               // [parts][nmax] partial sums
+  int* klist;                  // [nmax]
+  int* klist2;                 // [nmax]
+  uint32_t* cur;               // [pg][b][cbw_words]
+  uint32_t* win;               // [pg][hwin][bw_words] (+ phase copies at copy_words strides)
+};
+
+__device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan& pl) {
+  SmemLayout L;
+  L.tab = reinterpret_cast<double*>(base);
+  unsigned char* p = base + 256 * sizeof(double);
+  L.red64 = reinterpret_cast<unsigned long long*>(p);
+  p += kMaxSW * 8;
+  L.best_e = reinterpret_cast<double*>(p);
+  p += kMaxSW * 8;
+  L.best_k = reinterpret_cast<int*>(p);
+  p += kMaxSW * 4;
+  L.misc = reinterpret_cast<int*>(p);
+  p += 16 * 4;
+  L.miscd = reinterpret_cast<double*>(p);
+  p += 4 * 8;
+  L.bar = reinterpret_cast<unsigned long long*>(p);
+  L.sad = reinterpret_cast<uint32_t*>(base + pl.off_sad);
+  L.klist = reinterpret_cast<int*>(base + pl.off_klist);
+  L.klist2 = L.klist + pl.nmax;
+  L.cur = reinterpret_cast<uint32_t*>(base + pl.off_cur);
+  L.win = reinterpret_cast<uint32_t*>(base + pl.off_win);
+  return L;
+}
+
+static inline int smem_head_bytes() { return 256 * 8 + kMaxSW * 20 + 16 * 4 + 4 * 8 + 16; }
+
+// ---------------------------------------------------------------------------
+// TMA helpers (inline PTX)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// per-CTA context
+// ---------------------------------------------------------------------------
+template <typename Elem>
+struct PairCtx {
+  const Elem* cur;  // plane 0 of the current frame (global)
+  const Elem* ref;  // plane 0 of the reference frame (global)
+  int cur_z, ref_z; // first plane index of each frame in the tensor map's z dimension
+  int pitch;
+  long long plane_stride;
+  int frame_h, frame_w;  // candidate validity bounds
+  int P;
+  int max_value;
+  const double* tab;
+  double tol, lam, oml;
+};
+
+struct StageGeom {
+  int r, s, G, ncg;
+  int cx, cy;
+  int wx0, wy0;  // window origin in plane coordinates
+  int tx0;       // x of the staged box (wx0 rounded down to 16 bytes for TMA)
+  int d;         // wx0 - tx0: element offset of the window inside each staged row
+};
+
+__device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+// Fallback staging with plain loads (windows larger than a TMA box, or the
+// single-block search_stage API with arbitrary origins).  Rows are stored
+// unshifted relative to the window start (d == 0).
+template <typename Elem>
+__device__ void stage_ldg(const SmemLayout& L, const Elem* __restrict__ cur0, const Elem* __restrict__ ref0,
+                          int pitch, long long plane_stride, int frame_h, const StageGeom& g, int ox, int oy, int b,
+                          int npl, const StagePlan& pl) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  constexpr int SH = 8 * sizeof(Elem);
+  const int nt = blockDim.x;
+  const int bww = pl.bw / EPW;
+  const int row_max_w = pitch / EPW - 1;
+  const int total = npl * pl.hwin * bww;
+  for (int idx = threadIdx.x; idx < total; idx += nt) {
+    const int w = idx % bww;
+    const int row = (idx / bww) % pl.hwin;
+    const int pp = idx / (bww * pl.hwin);
+    const int gy = min(max(g.wy0 + row, 0), frame_h - 1);
+    const int gx = g.wx0 + w * EPW;
+    const int gw0 = floor_div(gx, EPW);
+    const int sh = gx - gw0 * EPW;
+    const uint32_t* row32 =
+        reinterpret_cast<const uint32_t*>(ref0 + (long long)pp * plane_stride + (long long)gy * pitch);
+    const uint32_t lo = __ldg(row32 + min(max(gw0, 0), row_max_w));
+    const uint32_t v = sh ? __funnelshift_r(lo, __ldg(row32 + min(max(gw0 + 1, 0), row_max_w)), sh * SH) : lo;
+    L.win[(pp * pl.wrows + row) * bww + w] = v;
+  }
+  const int cbw = pl.cbw / EPW, cw = b / EPW;
+  const int ctot = npl * b * cw;
+  for (int idx = threadIdx.x; idx < ctot; idx += nt) {
+    const int w = idx % cw;
+    const int row = (idx / cw) % b;
+    const int pp = idx / (cw * b);
+    const uint32_t* row32 =
+        reinterpret_cast<const uint32_t*>(cur0 + (long long)pp * plane_stride + (long long)(oy + row) * pitch);
+    const int gx = ox + w * EPW;
+    const int gw0 = gx / EPW;
+    const int sh = gx - gw0 * EPW;
+    const uint32_t lo = __ldg(row32 + gw0);
+    const uint32_t v = sh ? __funnelshift_r(lo, __ldg(row32 + gw0 + 1), sh * SH) : lo;
+    L.cur[(pp * b + row) * cbw + w] = v;
+  }
+}
+
+// Pre-shifted copies: copy f (1 <= f < EPW) holds every staged row advanced by
+// f elements, so a candidate whose window starts at element x reads copy
+// x % EPW at word x / EPW with plain aligned loads.  A thread turns one 16-byte
+// quad of a staged row (+ the next word) into the same quad of every needed
+// copy: 2 loads, one funnel shift per output word, one 16-byte store per copy.
+// The last word of a row takes its high bytes from the next row; that word is
+// slack (bw carries one spare word) and is never read by a candidate.
+template <typename Elem>
+__device__ void build_phase_copies(const SmemLayout& L, const StagePlan& pl, int npl, unsigned phase_mask) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  constexpr int SH = 8 * sizeof(Elem);
+  const int quads = npl * pl.wrows * (pl.bw / EPW) / 4;
+  const int nt = blockDim.x;
+  const int region1 = pl.copies == 2;  // single-phase stages keep their one copy in region 1
+  for (int qd = threadIdx.x; qd < quads; qd += nt) {
+    const uint4 v = reinterpret_cast<const uint4*>(L.win)[qd];
+    const uint32_t nx = L.win[4 * qd + 4];
+#pragma unroll
+    for (int f = 1; f < EPW; ++f) {
+      if (!(phase_mask & (1u << f))) continue;
+      uint4 o;
+      o.x = __funnelshift_r(v.x, v.y, f * SH);
+      o.y = __funnelshift_r(v.y, v.z, f * SH);
+      o.z = __funnelshift_r(v.z, v.w, f * SH);
+      o.w = __funnelshift_r(v.w, nx, f * SH);
+      reinterpret_cast<uint4*>(L.win + (region1 ? 1 : f) * pl.copy_words)[qd] = o;
+    }
+  }
+}
+
+template <int CW>
+__device__ __forceinline__ void load_cur(uint32_t (&dst)[CW], const uint32_t* src) {
+  if constexpr (CW == 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src);
+    dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+  } else {
+    const uint2 v = *reinterpret_cast<const uint2*>(src);
+    dst[0] = v.x; dst[1] = v.y;
+  }
+}
+
+// One reference row of CW words; with SHIFT the row starts `sh` bits into src[0].
+template <int CW, bool SHIFT>
+__device__ __forceinline__ void load_row(uint32_t (&dst)[CW], const uint32_t* src, int sh) {
+  if constexpr (SHIFT) {
+    uint32_t w[CW + 1];
+#pragma unroll
+    for (int q = 0; q <= CW; ++q) w[q] = src[q];
+#pragma unroll
+    for (int q = 0; q < CW; ++q) dst[q] = __funnelshift_r(w[q], w[q + 1], sh);
+  } else {
+#pragma unroll
+    for (int q = 0; q < CW; ++q) dst[q] = src[q];
+  }
+}
+
+// One step of the sliding window: block row m (ring slot of its new reference
+// row is (k + TY - 1) % TY), candidate j of the group pairs cur row m with
+// reference row m + j (slot (k + j) % TY).  K is the step's position in the
+// TY-period, so every ring index is a compile-time constant.
+template <typename Elem, int CW, int TY, bool SHIFT, int K>
+__device__ __forceinline__ void sad_step(uint32_t (&R)[TY][CW], uint32_t (&acc)[TY], const uint32_t*& rp,
+                                         const uint32_t*& cp, int rstep, int cstep, int sh) {
+  load_row<CW, SHIFT>(R[(K + TY - 1) % TY], rp, sh);
+  rp += rstep;
+  uint32_t C[CW];
+  load_cur<CW>(C, cp);
+  cp += cstep;
+#pragma unroll
+  for (int j = 0; j < TY; ++j) {
+#pragma unroll
+    for (int w = 0; w < CW; ++w) acc[j] = sad_word(C[w], R[(K + j) % TY][w], acc[j], Elem());
+  }
+}
+
+template <typename Elem, int CW, int TY, bool SHIFT, int K = 0>
+__device__ __forceinline__ void sad_period(uint32_t (&R)[TY][CW], uint32_t (&acc)[TY], const uint32_t*& rp,
+                                           const uint32_t*& cp, int rstep, int cstep, int sh) {
+  sad_step<Elem, CW, TY, SHIFT, K>(R, acc, rp, cp, rstep, cstep, sh);
+  if constexpr (K + 1 < TY) sad_period<Elem, CW, TY, SHIFT, K + 1>(R, acc, rp, cp, rstep, cstep, sh);
+}
+
+// Tail of fewer than TY steps: uniform early exit between steps (a branch, not
+// predication, so skipped steps issue nothing).
+template <typename Elem, int CW, int TY, bool SHIFT, int K = 0>
+__device__ __forceinline__ void sad_tail(uint32_t (&R)[TY][CW], uint32_t (&acc)[TY], const uint32_t*& rp,
+                                         const uint32_t*& cp, int rstep, int cstep, int sh, int rem) {
+  if constexpr (K + 1 < TY) {
+    if (K >= rem) return;
+    sad_step<Elem, CW, TY, SHIFT, K>(R, acc, rp, cp, rstep, cstep, sh);
+    sad_tail<Elem, CW, TY, SHIFT, K + 1>(R, acc, rp, cp, rstep, cstep, sh, rem);
+  }
+}
+
+// SAD of the TY candidates (rows gi*TY .. gi*TY+TY-1 of one column) over one
+// residue class of block rows (M rows, stride s).
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ __forceinline__ void sad_run(const uint32_t* rp, const uint32_t* cp, int rstep, int cstep, int M, int sh,
+                                        uint32_t (&acc)[TY]) {
+  uint32_t R[TY][CW];
+#pragma unroll
+  for (int k = 0; k < TY - 1; ++k) load_row<CW, SHIFT>(R[k], rp + k * rstep, sh);
+  rp += (TY - 1) * rstep;
+  int m0 = 0;
+  for (; m0 + TY <= M; m0 += TY) sad_period<Elem, CW, TY, SHIFT>(R, acc, rp, cp, rstep, cstep, sh);
+  if (m0 < M) sad_tail<Elem, CW, TY, SHIFT>(R, acc, rp, cp, rstep, cstep, sh, M - m0);
+}
+
+// Phase A: integer SAD of every (candidate column i, TY-row group gi, part)
+// item.  A part is a contiguous slice of the (plane, chunk, row residue) units; it owns the
+// partial-sum array L.sad[part][*].  `add` accumulates onto an earlier staging
+// pass (the item -> thread mapping is identical in every pass).
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int npl, const StagePlan& pl, int coff_w,
+                          bool add) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  const int nt = blockDim.x;
+  const int bww = pl.bw / EPW;
+  const int cbw = pl.cbw / EPW;
+  const int cpr = (b / EPW) / CW;
+  const int s = g.s;
+  const int nrho = s < b ? s : b;  // residue classes of block rows (independent sliding windows)
+  const int units = npl * cpr * nrho;
+  const int parts = pl.parts;
+  const int per = (units + parts - 1) / parts;
+  const int cols = g.G * g.ncg;
+  const int items = cols * parts;
+  const int rstep = s * bww, cstep = s * cbw;
+  const int N = g.G * g.G;
+  for (int it = threadIdx.x; it < items; it += nt) {
+    const int i = it % g.G;
+    const int q = it / g.G;
+    const int gi = q % g.ncg, part = q / g.ncg;
+    const int xo = g.d + i * s;
+    const int ph = xo % EPW;
+    const uint32_t* win = (SHIFT || ph == 0) ? L.win : L.win + (pl.copies == 2 ? 1 : ph) * pl.copy_words;
+    const int sh = ph * 8 * (int)sizeof(Elem);
+    uint32_t acc[TY];
+#pragma unroll
+    for (int j = 0; j < TY; ++j) acc[j] = 0;
+    const int u_end = min(units, (part + 1) * per);
+    for (int u = part * per; u < u_end; ++u) {
+      const int rho = u % nrho, pc = u / nrho;
+      const int pp = pc / cpr, c = pc - pp * cpr;
+      // window rows past hwin (next plane / slack rows) only feed the padding
+      // candidates of the last row group, whose sums are discarded.
+      const uint32_t* R0 = win + pp * pl.wrows * bww + (xo / EPW) + c * CW;
+      const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + c * CW;
+      const int M = (b - 1 - rho) / s + 1;
+      sad_run<Elem, CW, TY, SHIFT>(R0 + (rho + gi * TY * s) * bww, C0 + rho * cbw, rstep, cstep, M, sh, acc);
+    }
+    uint32_t* dst = L.sad + part * N;
+#pragma unroll
+    for (int j = 0; j < TY; ++j) {
+      const int jj = gi * TY + j;
+      if (jj < g.G) {
+        const int k = jj * g.G + i;
+        dst[k] = add ? dst[k] + acc[j] : acc[j];
+      }
+    }
+  }
+}
+
+struct StageResult {
+  int dx, dy;
+  double energy;
+  int nvalid;
+};
+
+__device__ __forceinline__ bool cand_valid_ij(const StageGeom& g, int ox, int oy, int b, int fh, int fw, int i, int j,
+                                              int& dx, int& dy) {
+  dx = g.cx + (i - g.r) * g.s;
+  dy = g.cy + (j - g.r) * g.s;
+  const int x = ox + dx, y = oy + dy;
+  return x >= 0 && x <= fw - b && y >= 0 && y <= fh - b;
+}
+
+// Exact energy of candidate (i, j).  When every plane is resident in shared
+// memory (pg == P) the replay reads the staged tiles; otherwise global memory.
+template <typename Elem>
+__device__ __forceinline__ double exact_cand(const SmemLayout& L, const StagePlan& pl, const StageGeom& g,
+                                             const PairCtx<Elem>& pc, int ox, int oy, int b, int coff, int i, int j,
+                                             int dx, int dy) {
+  if (pl.pg == pc.P) {
+    const Elem* cur = reinterpret_cast<const Elem*>(L.cur) + coff;
+    const Elem* ref = reinterpret_cast<const Elem*>(L.win) + (long long)(j * g.s) * pl.bw + g.d + i * g.s;
+    return exact_energy_generic<Elem>(cur, pl.cbw, (long long)b * pl.cbw, ref, pl.bw, (long long)pl.wrows * pl.bw, b,
+                                      pc.P, pc.tab, pc.tol, pc.oml, pc.lam)
+        .energy;
+  }
+  const long long roff = (long long)(oy + dy) * pc.pitch + (ox + dx);
+  const long long coffg = (long long)oy * pc.pitch + ox;
+  return exact_energy_generic<Elem>(pc.cur + coffg, pc.pitch, pc.plane_stride, pc.ref + roff, pc.pitch,
+                                    pc.plane_stride, b, pc.P, pc.tab, pc.tol, pc.oml, pc.lam)
+      .energy;
+}
+
+// Integer lower bound of the sparsity count of candidate (i, j): #(|r-c| >= D),
+// warp-cooperative over packed 32-bit words (staged tiles, or global planes
+// when not every plane is staged).  uint8: one VABSDIFF4 (per-byte |r-c|) and
+// two VABSDIFF4.ACC against D-1 and D, using [d >= D] = (|d-(D-1)| - |d-D| + 1)/2
+// for integers.  uint16: per-lane |r-c| = max - min (VIMNMX.U16x2), then the
+// lane's bit 15 is set iff d >= D (7-bit-carry-free add), counted with POPC.
+template <typename Elem>
+__device__ __forceinline__ uint32_t ldw_shifted(const uint32_t* base, int elem) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  const int w = elem / EPW, sh = elem % EPW;  // elem >= 0
+  const uint32_t lo = base[w];
+  return sh ? __funnelshift_r(lo, base[w + 1], sh * 8 * (int)sizeof(Elem)) : lo;
+}
+
+template <typename Elem>
+__device__ int count_lo(const SmemLayout& L, const StagePlan& pl, const StageGeom& g, const PairCtx<Elem>& pc,
+                        int ox, int oy, int b, int coff, int i, int j, int D) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  const int lane = threadIdx.x & 31;
+  const int n = pc.P * b * b;
+  if (D > pc.max_value) return 0;
+  const int lb = __ffs(b) - 1;
+  const int lwpr = lb - (EPW == 4 ? 2 : 1);  // log2(words per block row)
+  const int words = n / EPW;
+  const bool staged = pl.pg == pc.P;
+  const int dx = g.cx + (i - g.r) * g.s, dy = g.cy + (j - g.r) * g.s;
+  uint32_t a1 = 0, a2 = 0;
+  int cnt = 0;
+  uint32_t k1, k2;
+  if constexpr (EPW == 4) {
+    k1 = 0x01010101u * (uint32_t)(D - 1);
+    k2 = 0x01010101u * (uint32_t)D;
+  } else {
+    k1 = D <= 32768 ? 0x00010001u * (uint32_t)(0x8000 - D) : 0x00010001u * (uint32_t)(0x10000 - D);
+    k2 = 0;
+  }
+  for (int t = lane; t < words; t += 32) {
+    const int wc = t & ((1 << lwpr) - 1), y = (t >> lwpr) & (b - 1), p = t >> (lwpr + lb);
+    uint32_t cw, rw;
+    if (staged) {
+      cw = ldw_shifted<Elem>(L.cur, (p * b + y) * pl.cbw + coff + wc * EPW);
+      rw = ldw_shifted<Elem>(L.win, (p * pl.wrows + j * g.s + y) * pl.bw + g.d + i * g.s + wc * EPW);
+    } else {
+      const uint32_t* crow = reinterpret_cast<const uint32_t*>(pc.cur + p * pc.plane_stride +
+                                                               (long long)(oy + y) * pc.pitch);
+      const uint32_t* rrow = reinterpret_cast<const uint32_t*>(pc.ref + p * pc.plane_stride +
+                                                               (long long)(oy + dy + y) * pc.pitch);
+      cw = ldw_shifted<Elem>(crow, ox + wc * EPW);
+      rw = ldw_shifted<Elem>(rrow, ox + dx + wc * EPW);
+    }
+    if constexpr (EPW == 4) {
+      const uint32_t d4 = __vabsdiffu4(cw, rw);
+      asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(d4), "r"(k1));
+      asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a2) : "r"(d4), "r"(k2));
+    } else {
+      uint32_t mx, mn;
+      asm("max.u16x2 %0, %1, %2;" : "=r"(mx) : "r"(cw), "r"(rw));
+      asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(cw), "r"(rw));
+      const uint32_t d2 = mx - mn;
+      const uint32_t f = D <= 32768 ? (((d2 & 0x7fff7fffu) + k1) | d2) : (((d2 & 0x7fff7fffu) + k1) & d2);
+      cnt += __popc(f & 0x80008000u);
+    }
+  }
+  if constexpr (EPW == 4) cnt = (int)a1 - (int)a2;
+  for (int m = 16; m; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
+  return EPW == 4 ? (cnt + n) / 2 : cnt;
+}
+
+// One stage for one block; all threads participate and receive the result.
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
+                                    const CUtensorMap* tm_win, const CUtensorMap* tm_cur, uint32_t& phase, int ox,
+                                    int oy, int b, int cx, int cy, int r, int s) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  StageGeom g;
+  g.r = r;
+  g.s = s;
+  g.G = 2 * r + 1;
+  g.ncg = (g.G + TY - 1) / TY;
+  g.cx = cx;
+  g.cy = cy;
+  g.wx0 = ox + cx - r * s;
+  g.wy0 = oy + cy - r * s;
+  // TMA tile loads need the box's inner start coordinate on a 16-byte boundary
+  constexpr int A16 = 16 / (int)sizeof(Elem);
+  g.tx0 = pl.use_tma ? g.wx0 - (((g.wx0 % A16) + A16) % A16) : g.wx0;
+  g.d = g.wx0 - g.tx0;
+  const int cx0 = pl.use_tma ? ox - (ox % A16) : ox;  // ox >= 0
+  const int coff_w = (ox - cx0) / EPW;
+  const int coff_e = ox - cx0;  // element offset of the block inside each staged cur row
+  const int N = g.G * g.G;
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = pc.P * b * b;
+  // sub-word phases used by this CTA's candidate columns
+  unsigned phase_mask = 0;
+  if (!SHIFT && pl.copies)
+    for (int i = 0; i < min(g.G, EPW); ++i) phase_mask |= 1u << ((g.d + i * s) % EPW);
+
+  __syncthreads();  // previous users of smem are done; mbarrier init visible
+  for (int p0 = 0; p0 < pc.P; p0 += pl.pg) {
+    const int npl = min(pl.pg, pc.P - p0);
+    if (p0) __syncthreads();
+    if (pl.use_tma) {
+      if (tid == 0) {
+        mbar_expect_tx(L.bar, (uint32_t)(pl.tma_bytes));  // full boxes, OOB included
+        tma_load_3d(L.win, tm_win, g.tx0, g.wy0, pc.ref_z + p0, L.bar);
+        tma_load_3d(L.cur, tm_cur, cx0, oy, pc.cur_z + p0, L.bar);
+      }
+      mbar_wait(L.bar, phase);
+      phase ^= 1;
+    } else {
+      stage_ldg<Elem>(L, pc.cur + (long long)p0 * pc.plane_stride, pc.ref + (long long)p0 * pc.plane_stride, pc.pitch,
+                      pc.plane_stride, pc.frame_h, g, ox, oy, b, npl, pl);
+    }
+    if (phase_mask & ~1u) {
+      __syncthreads();
+      build_phase_copies<Elem>(L, pl, npl, phase_mask);
+    }
+    __syncthreads();
+    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0);
+  }
+  __syncthreads();
+
+  // valid candidates form a rectangle i in [ilo, ihi] x j in [jlo, jhi] (fme.py:250-253)
+  const int ilo = max(0, r - floor_div(ox + cx, s)), ihi = min(g.G - 1, r + floor_div(pc.frame_w - b - ox - cx, s));
+  const int jlo = max(0, r - floor_div(oy + cy, s)), jhi = min(g.G - 1, r + floor_div(pc.frame_h - b - oy - cy, s));
+  const int wi = ihi - ilo + 1, wj = jhi - jlo + 1;
+  StageResult res;
+  res.nvalid = (wi > 0 && wj > 0) ? wi * wj : 0;
+  if (res.nvalid == 0) {
+    res.dx = res.dy = 0;
+    res.energy = 0.0;
+    return res;
+  }
+
+  // pass 1: fold the parts; first minimum SAD among valid candidates (key = sad<<32 | k)
+  unsigned long long best = ~0ull;
+  {
+    const int parts = pl.parts;
+    for (int v = tid; v < res.nvalid; v += nt) {
+      const int jv = v / wi;
+      const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
+      uint32_t sk = L.sad[k];
+      for (int q = 1; q < parts; ++q) sk += L.sad[q * N + k];
+      if (parts > 1) L.sad[k] = sk;  // the contender passes read the folded sums
+      const unsigned long long key = ((unsigned long long)sk << 32) | (unsigned)k;
+      best = key < best ? key : best;
+    }
+  }
+  for (int m = 16; m; m >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, m);
+    best = o < best ? o : best;
+  }
+  if (lane == 0) L.red64[warp] = best;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long b0 = L.red64[0];
+    for (int w = 1; w < nw; ++w) b0 = L.red64[w] < b0 ? L.red64[w] : b0;
+    L.misc[0] = (int)(b0 & 0xffffffffu);
+    L.misc[2] = (int)(b0 >> 32);
+    L.misc[3] = 0;  // klist size
+    L.misc[5] = 0;  // replay list size
+  }
+  __syncthreads();
+  const int m0 = L.misc[0];
+  const unsigned sad0 = (unsigned)L.misc[2];
+  if (sad0 == 0 && pc.oml > 0.0) {
+    // S == 0 gives E == 0.0 exactly; any earlier candidate has S > 0 and,
+    // with (1-lam) > 0, E > 0.  The first zero-SAD candidate wins.
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, res.dx, res.dy);
+    res.energy = 0.0;
+    return res;
+  }
+  if (sizeof(Elem) == 1)  // fl(v/255) table for the exact replays (only blocks that reach here pay for it)
+    for (int v = tid; v < 256; v += nt) L.tab[v] = __ddiv_rn((double)v, (double)pc.max_value);
+  __syncthreads();
+  const double unit = (double)pc.max_value * (double)n;
+  if (warp == 0) {
+    double e0 = 0.0;
+    if (sad0 != 0) {
+      int dx, dy;
+      cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, dx, dy);
+      e0 = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, m0 % g.G, m0 / g.G, dx, dy);
+    }
+    if (lane == 0) {
+      L.miscd[0] = e0;
+      // integer SAD threshold: the largest S whose bound (1-lam)*S/(s*n) can
+      // still reach e0 + eps (the bound is monotone in S)
+      const double lim = e0 + kScreenEps;
+      unsigned thr = 0xffffffffu;
+      if (pc.oml > 0.0) {
+        double est = floor(lim / pc.oml * unit) + 2.0;
+        long long t = est > 4294967295.0 ? 4294967295LL : (long long)est;
+        while (t >= 0 && __dmul_rn(pc.oml, __ddiv_rn((double)t, unit)) > lim) --t;
+        thr = t < 0 ? 0u : (unsigned)t;
+      }
+      L.misc[6] = (int)thr;
+    }
+  }
+  __syncthreads();
+  const double e0 = L.miscd[0];
+  const unsigned sthr = (unsigned)L.misc[6];
+  // pass 2: SAD contenders (candidates whose lower bound reaches e0)
+  for (int v = tid; v < res.nvalid; v += nt) {
+    const int jv = v / wi;
+    const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
+    if (k != m0 && L.sad[k] <= sthr) L.klist[atomicAdd(&L.misc[3], 1)] = k;
+  }
+  __syncthreads();
+  int nk = L.misc[3];
+  const int* rlist = L.klist;
+  if (nk > nw && pc.lam > 0.0) {
+    // Too many for one round of float64 replays: tighten the bound with the
+    // sparsity term.  C_lo = #(|r-c| >= D) <= C because every integer
+    // difference >= D passes the float64 test d > tol; then
+    // E >= (1-lam)*S/(s*n) + lam*C_lo/n (up to float rounding << eps).
+    const int D = (int)floor(pc.tol * (double)pc.max_value + 1e-9) + 1;
+    const double lim = e0 + kScreenEps;
+    for (int e = warp; e < nk; e += nw) {
+      const int k = L.klist[e];
+      const int clo = count_lo<Elem>(L, pl, g, pc, ox, oy, b, coff_e, k % g.G, k / g.G, D);
+      const double elb = __dadd_rn(__dmul_rn(pc.oml, __ddiv_rn((double)L.sad[k], unit)),
+                                   __dmul_rn(pc.lam, __ddiv_rn((double)clo, (double)n)));
+      if (lane == 0 && elb - kScreenEps <= lim) L.klist2[atomicAdd(&L.misc[5], 1)] = k;
+    }
+    __syncthreads();
+    nk = L.misc[5];
+    rlist = L.klist2;
+  }
+  double be = (warp == 0) ? e0 : 1e300;
+  int bk = (warp == 0) ? m0 : 0x7fffffff;
+  for (int e = warp; e < nk; e += nw) {
+    const int k = rlist[e];
+    int dx, dy;
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, k % g.G, k / g.G, dx, dy);
+    const double ek = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, k % g.G, k / g.G, dx, dy);
+    if (ek < be || (ek == be && k < bk)) {
+      be = ek;
+      bk = k;
+    }
+  }
+  if (lane == 0) {
+    L.best_e[warp] = be;
+    L.best_k[warp] = bk;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double e = L.best_e[0];
+    int k = L.best_k[0];
+    for (int w = 1; w < nw; ++w) {
+      if (L.best_e[w] < e || (L.best_e[w] == e && L.best_k[w] < k)) {
+        e = L.best_e[w];
+        k = L.best_k[w];
+      }
+    }
+    L.misc[4] = k;
+    L.miscd[1] = e;
+  }
+  __syncthreads();
+  const int kw = L.misc[4];
+  cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, kw % g.G, kw / g.G, res.dx, res.dy);
+  res.energy = L.miscd[1];
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// the stage kernel
+// ---------------------------------------------------------------------------
+template <typename Elem, int CW, int TY, bool SHIFT>
+__global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
+    fme_stage_kernel(const __grid_constant__ CUtensorMap tm_win, const __grid_constant__ CUtensorMap tm_cur,
+                     const StageLaunch a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const SmemLayout L = carve(smem_raw, a.plan);
+  const bmc_fme_params& p = a.prm;
+  const int b = a.b;
+  int pair = 0, gx = 0, gy = 0, ox, oy, sx = 0, sy = 0;
+  long long cell = 0;
+  if (a.single) {
+    ox = a.ox;
+    oy = a.oy;
+    sx = a.cx;
+    sy = a.cy;
+  } else {
+    const int blk = blockIdx.x;
+    pair = blockIdx.y;
+    gx = blk % a.gw;
+    gy = blk / a.gw;
+    cell = (long long)pair * a.gw * a.gh + blk;
+    ox = gx * b;
+    oy = gy * b;
+    if (a.level > 0) {
+      const int pgw = a.gw / 2, pgh = a.gh / 2;
+      const long long pcell = (long long)pair * pgw * pgh + (gy / 2) * pgw + (gx / 2);
+      if (a.parent_matched[pcell]) {  // inherited: copy the parent (fme.py:352-362)
+        if (a.first && threadIdx.x == 0) {
+          a.mv[2 * cell] = a.parent_mv[2 * pcell];
+          a.mv[2 * cell + 1] = a.parent_mv[2 * pcell + 1];
+          a.energy[cell] = a.parent_e[pcell];
+          a.matched[cell] = 1;
+        }
+        return;
+      }
+      if (a.first) {
+        sx = a.parent_mv[2 * pcell];
+        sy = a.parent_mv[2 * pcell + 1];
+      }
+    }
+    if (!a.first) {
+      sx = a.mv[2 * cell];
+      sy = a.mv[2 * cell + 1];
+    }
+  }
+  PairCtx<Elem> pc;
+  const int cur_f = a.single ? 0 : a.cur_index[pair];
+  const int ref_f = a.single ? 0 : a.ref_index[pair];
+  pc.cur = reinterpret_cast<const Elem*>(a.planes) + (long long)cur_f * p.frame_stride;
+  pc.ref = reinterpret_cast<const Elem*>(a.ref_planes) + (long long)ref_f * p.frame_stride;
+  pc.cur_z = cur_f * p.planes;
+  pc.ref_z = ref_f * p.planes;
+  pc.pitch = p.pitch;
+  pc.plane_stride = p.plane_stride;
+  pc.frame_h = a.single ? p.real_h : p.pad_h;  // search_stage works on unpadded planes (fme.py:279-284)
+  pc.frame_w = a.single ? p.real_w : p.pad_w;
+  pc.P = p.planes;
+  pc.max_value = p.max_value;
+  pc.tol = p.sparsity_tolerance;
+  pc.lam = p.lam;
+  pc.oml = p.one_minus_lam;
+  pc.tab = sizeof(Elem) == 1 ? L.tab : a.tab16;  // the uint8 table is filled lazily (first exact replay)
+  uint32_t phase = 0;
+  if (a.plan.use_tma && threadIdx.x == 0) mbar_init(L.bar, 1);
+  StageResult res;
+  for (int attempt = 0;; ++attempt) {  // no valid candidate: re-centre on (0, 0) (fme.py:310-313)
+    res = stage_search<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox, oy, b, attempt ? 0 : sx,
+                                            attempt ? 0 : sy, a.r, a.s);
+    if (res.nvalid || attempt) break;
+  }
+  if (threadIdx.x != 0) return;
+  if (a.single) {
+    a.mv[0] = res.dx;
+    a.mv[1] = res.dy;
+    a.energy[0] = res.energy;
+    a.nvalid_out[0] = res.nvalid;
+    return;
+  }
+  a.mv[2 * cell] = res.dx;
+  a.mv[2 * cell + 1] = res.dy;
+  a.energy[cell] = res.energy;
+  if (a.last) {
+    bool m;
+    if (a.final_level) {
+      const bool in_real = oy < p.real_h && ox < p.real_w;  // fme.py:377-384
+      m = !(res.energy > p.refine_block_threshold && in_real);
+    } else {
+      m = res.energy <= p.split_threshold;  // fme.py:386
+    }
+    a.matched[cell] = m ? 1 : 0;
+  }
+  atomicAdd(a.evals + pair, (unsigned long long)(res.nvalid + a.extra_evals));
+}
+
+template <typename K>
+inline int set_smem(K kern, int bytes) {
+  // cudaFuncSetAttribute is cheap but not free (and best kept out of graph
+  // capture): remember the largest value set per instantiation.
+  static std::mutex mu;
+  static const void* keys[512];
+  static int vals[512];
+  static int n = 0;
+  std::lock_guard<std::mutex> g(mu);
+  const void* key = reinterpret_cast<const void*>(kern);
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == key) {
+      if (vals[i] >= bytes) return BMC_OK;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+      vals[i] = bytes;
+      return BMC_OK;
+    }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+  if (n < 512) {
+    keys[n] = key;
+    vals[n] = bytes;
+    ++n;
+  }
+  return BMC_OK;
+}
+
+inline bool sync_debug() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BMC_SYNC_DEBUG");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <typename E, int CW, int TY, bool SH>
+inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid, cudaStream_t st) {
+  int rc = set_smem(fme_stage_kernel<E, CW, TY, SH>, a.plan.smem);
+  if (rc) return rc;
+  static const bool plan_log = [] {
+    const char* e = getenv("BMC_PLAN_LOG");
+    return e && *e && *e != '0';
+  }();
+  if (plan_log)
+    fprintf(stderr, "[bmc] stage eb=%d CW=%d TY=%d shift=%d level %d b %d r %d s %d grid %ux%u threads %d parts %d "
+            "pg %d tma %d box %dx%d copies %d smem %d\n", (int)sizeof(E), CW, TY, (int)SH, a.level, a.b, a.r, a.s,
+            grid.x, grid.y, a.plan.threads, a.plan.parts, a.plan.pg, a.plan.use_tma, a.plan.bw, a.plan.hwin,
+            a.plan.copies, a.plan.smem);
+  fme_stage_kernel<E, CW, TY, SH><<<grid, a.plan.threads, a.plan.smem, st>>>(tw, tc, a);
+  rc = cuda_status(cudaGetLastError(), "fme_stage_kernel");
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!rc && sync_debug() && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error("fme_stage_kernel<eb=%d,CW=%d,TY=%d,shift=%d> level %d b %d r %d s %d tma %d box %dx%dx%d cbw %d "
+                "smem %d threads %d parts %d copies %d: %s", (int)sizeof(E), CW, TY, (int)SH, a.level, a.b, a.r, a.s,
+                a.plan.use_tma, a.plan.bw, a.plan.hwin, a.plan.pg, a.plan.cbw, a.plan.smem, a.plan.threads,
+                a.plan.parts, a.plan.copies, cudaGetErrorString(e));
+      return BMC_E_CUDA;
+    }
+  }
+  return rc;
+}
+
+template <typename E, int CW, bool SH>
+inline int dispatch_ty(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid,
+                       cudaStream_t st) {
+  switch (a.plan.ty) {
+    case 1: return launch_one<E, CW, 1, SH>(tw, tc, a, grid, st);
+    case 2: return launch_one<E, CW, 2, SH>(tw, tc, a, grid, st);
+    case 3: return launch_one<E, CW, 3, SH>(tw, tc, a, grid, st);
+    case 4: return launch_one<E, CW, 4, SH>(tw, tc, a, grid, st);
+    case 5: return launch_one<E, CW, 5, SH>(tw, tc, a, grid, st);
+    case 6: return launch_one<E, CW, 6, SH>(tw, tc, a, grid, st);
+    case 7: return launch_one<E, CW, 7, SH>(tw, tc, a, grid, st);
+    case 8: return launch_one<E, CW, 8, SH>(tw, tc, a, grid, st);
+    case 9: return launch_one<E, CW, 9, SH>(tw, tc, a, grid, st);
+    case 10: return launch_one<E, CW, 10, SH>(tw, tc, a, grid, st);
+    case 11: return launch_one<E, CW, 11, SH>(tw, tc, a, grid, st);
+    default: return launch_one<E, CW, 12, SH>(tw, tc, a, grid, st);
+  }
+}
+
+
+// One translation unit per (element type, chunk width, shift) instantiates its
+// twelve TY variants (bmc_fme_k_*.cu), so the build compiles them in parallel.
+int launch_stage_u8c4(bool shift, const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid,
+                      cudaStream_t st);
+int launch_stage_u8c2(bool shift, const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid,
+                      cudaStream_t st);
+int launch_stage_u16(bool shift, const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid,
+                     cudaStream_t st);
+
+}  // namespace bmc

@@ -9,8 +9,12 @@ namespace bmc {
 // Host-computed plan of one search-stage launch (shared-memory layout, TMA boxes).
 struct StagePlan {
   int ty;         // candidate rows per thread (template parameter TY)
-  int parts;      // (plane, chunk) slices per candidate column group (1 = no atomics)
-  int shift;      // sub-word candidate offsets need a funnel shift
+  int parts;      // (plane, chunk) slices per candidate column group; each owns a partial-sum array
+  int threads;    // CTA size (multiple of 32, <= kMaxStageThreads)
+  int shift;      // 1: sub-word candidate offsets funnel-shifted in the inner loop (template SHIFT)
+  int copies;     // sub-word phases served from pre-shifted window copies built once per stage:
+                  // 0 none, 1 one region per phase, 2 one region (the stage uses a single phase)
+  int copy_words; // distance between phase copies (32-bit words; bank-skewed)
   int nmax;       // candidates (2r+1)^2
   int pg;         // planes staged per pass
   int bw;         // window box width (elements; 16-byte multiple, +1 word slack)
@@ -22,6 +26,11 @@ struct StagePlan {
   int off_sad, off_klist, off_cur, off_win;
   int smem;
 };
+
+#ifndef BMC_STAGE_THREADS
+#define BMC_STAGE_THREADS 416
+#endif
+constexpr int kMaxStageThreads = BMC_STAGE_THREADS;  // max CTA size of the search kernel
 
 struct StageLaunch {
   const void* planes;       // current-frame plane buffer

@@ -1,12 +1,15 @@
 #!/bin/bash
-# Build search-kernel CTA-shape variants into tools/variants/<name>/libbmc_b200.so
-set -e
-cd "$(dirname "$0")/.."
-for v in "256 2" "128 4" "256 3" "128 3" "384 1" "192 2"; do
-  set -- $v
-  d=tools/variants/t$1_b$2; mkdir -p $d
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --shared -Xcompiler -fPIC \
-    -DBMC_SEARCH_THREADS=$1 -DBMC_SEARCH_MINB=$2 -I include -o $d/libbmc_b200.so \
-    paper_2508_05990_b200/csrc/bmc_api.cu paper_2508_05990_b200/csrc/bmc_fme.cu paper_2508_05990_b200/csrc/bmc_ops.cu &
+# Build search-kernel variants (CTA size / min resident CTAs) into tools/variants/<name>/libbmc_b200.so
+# usage: tools/build_variants.sh name:THREADS:MINB [...]
+cd "$(dirname "$0")/../paper_2508_05990_b200/csrc"
+for spec in "$@"; do
+  IFS=: read name th mb <<< "$spec"
+  out=/root/repo/tools/variants/$name; mkdir -p $out /tmp/vobj_$name
+  ( for f in bmc_api bmc_fme bmc_fme_k_u8c4 bmc_fme_k_u8c2 bmc_fme_k_u16 bmc_ops; do
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+        -DBMC_STAGE_THREADS=$th -DBMC_STAGE_MINB=$mb -I ../../include -c $f.cu -o /tmp/vobj_$name/$f.o &
+    done; wait
+    nvcc -gencode arch=compute_100a,code=sm_100a --shared -o $out/libbmc_b200.so /tmp/vobj_$name/*.o ) &
 done
 wait
+ls -la /root/repo/tools/variants/*/

@@ -1,9 +1,10 @@
 #!/bin/bash
+# Time the ME launch of each config with the in-tree library and every tools/variants/*/libbmc_b200.so.
+# usage: tools/run_variants.sh "c2 c5" [reps]
 cd "$(dirname "$0")/.."
-python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -1
+cfgs=${1:-c2}; reps=${2:-8}
+for c in $cfgs; do VARIANT=default timeout 300 python tools/time_me.py $c $reps 2>&1 | tail -1; done
 for d in tools/variants/*/; do
   n=$(basename $d)
-  for ty in 12 11 8 6; do
-    VARIANT=$n BMC_TY_MAX=$ty BMC_LIB_PATH=$PWD/$d/libbmc_b200.so python tools/time_me.py c2 8 2>/dev/null
-  done
+  for c in $cfgs; do VARIANT=$n BMC_LIB_PATH=$PWD/$d/libbmc_b200.so timeout 300 python tools/time_me.py $c $reps 2>&1 | tail -1; done
 done
