@@ -204,6 +204,7 @@ int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* 
       a.b = b;
       a.gw = p->pad_w / b;
       a.gh = p->pad_h / b;
+      a.n_pairs = n_pairs;
       a.first = k == 0;
       a.last = k == nl - 1;
       a.r = p->stage_range[s];
@@ -402,6 +403,46 @@ int bmc_predict_labels(uint8_t* labels, int64_t frame_stride, int64_t stream_str
   a.B = B;
   a.scale = scale;
   return launch_predict(a, n_streams, (cudaStream_t)stream);
+}
+
+int bmc_predict_labels_clip(uint8_t* labels, int64_t frame_stride, int64_t stream_stride, const uint8_t* key_labels,
+                            int n_streams, int t_begin, int t_end, const int32_t* kind, const int32_t* ref,
+                            int64_t kind_stream_stride, int height, int width, const int32_t* mv,
+                            int64_t mv_frame_stride, int64_t mv_stream_stride, int grid_h, int grid_w, int block_size,
+                            int scale, uint32_t* workspace, void* stream) {
+  if (!labels || !mv || !kind || !ref || !key_labels || !workspace || n_streams < 0) {
+    set_error("NULL argument");
+    return BMC_E_ARG;
+  }
+  if (scale != 1 && scale != 2) {
+    set_error("scale must be 1 or 2");
+    return BMC_E_ARG;
+  }
+  const int B = block_size * scale;
+  if (grid_w * B < width || grid_h * B < height) {
+    set_error("motion field covers %dx%d, labels are %dx%d", grid_w * B, grid_h * B, width, height);
+    return BMC_E_ARG;
+  }
+  if (n_streams == 0 || height == 0 || width == 0 || t_end <= t_begin) return BMC_OK;
+  PredictArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.labels = labels;
+  a.fs = frame_stride;
+  a.ss = stream_stride;
+  a.key_labels = key_labels;
+  a.kind = kind;
+  a.ref = ref;
+  a.kss = kind_stream_stride;
+  a.H = height;
+  a.W = width;
+  a.mv = mv;
+  a.mvfs = mv_frame_stride;
+  a.mvss = mv_stream_stride;
+  a.gh = grid_h;
+  a.gw = grid_w;
+  a.B = B;
+  a.scale = scale;
+  return launch_predict_chain(a, n_streams, t_begin, t_end, workspace, (cudaStream_t)stream);
 }
 
 int bmc_predict_features(const float* ref_feats, float* out_feats, int channels, int height, int width,

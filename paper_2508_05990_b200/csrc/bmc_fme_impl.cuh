@@ -165,6 +165,18 @@ struct StageGeom {
 
 __device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
+// Division by a CTA-uniform divisor without the ~20-instruction integer divide:
+// q = umulhi(n, floor(2^32/d) + 1) is exact for n, d < 2^16.
+struct FastDiv {
+  uint32_t d, m;
+  __device__ __forceinline__ explicit FastDiv(uint32_t d_) : d(d_), m(d_ > 1 ? 0xffffffffu / d_ + 1u : 0u) {}
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return d > 1 ? __umulhi(n, m) : n; }
+  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
+    q = div(n);
+    r = n - q * d;
+  }
+};
+
 // Fallback staging with plain loads (windows larger than a TMA box, or the
 // single-block search_stage API with arbitrary origins).  Rows are stored
 // unshifted relative to the window start (d == 0).
@@ -338,10 +350,11 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   const int items = cols * parts;
   const int rstep = s * bww, cstep = s * cbw;
   const int N = g.G * g.G;
+  const FastDiv fG(g.G), fncg(g.ncg), frho(nrho), fcpr(cpr), fs(s);
   for (int it = threadIdx.x; it < items; it += nt) {
-    const int i = it % g.G;
-    const int q = it / g.G;
-    const int gi = q % g.ncg, part = q / g.ncg;
+    uint32_t q, i, gi, part;
+    fG.divmod(it, q, i);
+    fncg.divmod(q, part, gi);
     const int xo = g.d + i * s;
     const int ph = xo % EPW;
     const uint32_t* win = (SHIFT || ph == 0) ? L.win : L.win + (pl.copies == 2 ? 1 : ph) * pl.copy_words;
@@ -351,13 +364,14 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
     for (int j = 0; j < TY; ++j) acc[j] = 0;
     const int u_end = min(units, (part + 1) * per);
     for (int u = part * per; u < u_end; ++u) {
-      const int rho = u % nrho, pc = u / nrho;
-      const int pp = pc / cpr, c = pc - pp * cpr;
+      uint32_t rho, pc, pp, c;
+      frho.divmod(u, pc, rho);
+      fcpr.divmod(pc, pp, c);
       // window rows past hwin (next plane / slack rows) only feed the padding
       // candidates of the last row group, whose sums are discarded.
       const uint32_t* R0 = win + pp * pl.wrows * bww + (xo / EPW) + c * CW;
       const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + c * CW;
-      const int M = (b - 1 - rho) / s + 1;
+      const int M = (int)fs.div(b - 1 - rho) + 1;
       sad_run<Elem, CW, TY, SHIFT>(R0 + (rho + gi * TY * s) * bww, C0 + rho * cbw, rstep, cstep, M, sh, acc);
     }
     uint32_t* dst = L.sad + part * N;
@@ -542,12 +556,13 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
     return res;
   }
 
+  const FastDiv fwi(wi);
   // pass 1: fold the parts; first minimum SAD among valid candidates (key = sad<<32 | k)
   unsigned long long best = ~0ull;
   {
     const int parts = pl.parts;
     for (int v = tid; v < res.nvalid; v += nt) {
-      const int jv = v / wi;
+      const int jv = fwi.div(v);
       const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
       uint32_t sk = L.sad[k];
       for (int q = 1; q < parts; ++q) sk += L.sad[q * N + k];
@@ -611,7 +626,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   const unsigned sthr = (unsigned)L.misc[6];
   // pass 2: SAD contenders (candidates whose lower bound reaches e0)
   for (int v = tid; v < res.nvalid; v += nt) {
-    const int jv = v / wi;
+    const int jv = fwi.div(v);
     const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
     if (k != m0 && L.sad[k] <= sthr) L.klist[atomicAdd(&L.misc[3], 1)] = k;
   }
@@ -683,90 +698,97 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
   const SmemLayout L = carve(smem_raw, a.plan);
   const bmc_fme_params& p = a.prm;
   const int b = a.b;
-  int pair = 0, gx = 0, gy = 0, ox, oy, sx = 0, sy = 0;
-  long long cell = 0;
-  if (a.single) {
-    ox = a.ox;
-    oy = a.oy;
-    sx = a.cx;
-    sy = a.cy;
-  } else {
-    const int blk = blockIdx.x;
-    pair = blockIdx.y;
-    gx = blk % a.gw;
-    gy = blk / a.gw;
-    cell = (long long)pair * a.gw * a.gh + blk;
-    ox = gx * b;
-    oy = gy * b;
-    if (a.level > 0) {
-      const int pgw = a.gw / 2, pgh = a.gh / 2;
-      const long long pcell = (long long)pair * pgw * pgh + (gy / 2) * pgw + (gx / 2);
-      if (a.parent_matched[pcell]) {  // inherited: copy the parent (fme.py:352-362)
-        if (a.first && threadIdx.x == 0) {
-          a.mv[2 * cell] = a.parent_mv[2 * pcell];
-          a.mv[2 * cell + 1] = a.parent_mv[2 * pcell + 1];
-          a.energy[cell] = a.parent_e[pcell];
-          a.matched[cell] = 1;
-        }
-        return;
-      }
-      if (a.first) {
-        sx = a.parent_mv[2 * pcell];
-        sy = a.parent_mv[2 * pcell + 1];
-      }
-    }
-    if (!a.first) {
-      sx = a.mv[2 * cell];
-      sy = a.mv[2 * cell + 1];
-    }
-  }
-  PairCtx<Elem> pc;
-  const int cur_f = a.single ? 0 : a.cur_index[pair];
-  const int ref_f = a.single ? 0 : a.ref_index[pair];
-  pc.cur = reinterpret_cast<const Elem*>(a.planes) + (long long)cur_f * p.frame_stride;
-  pc.ref = reinterpret_cast<const Elem*>(a.ref_planes) + (long long)ref_f * p.frame_stride;
-  pc.cur_z = cur_f * p.planes;
-  pc.ref_z = ref_f * p.planes;
-  pc.pitch = p.pitch;
-  pc.plane_stride = p.plane_stride;
-  pc.frame_h = a.single ? p.real_h : p.pad_h;  // search_stage works on unpadded planes (fme.py:279-284)
-  pc.frame_w = a.single ? p.real_w : p.pad_w;
-  pc.P = p.planes;
-  pc.max_value = p.max_value;
-  pc.tol = p.sparsity_tolerance;
-  pc.lam = p.lam;
-  pc.oml = p.one_minus_lam;
-  pc.tab = sizeof(Elem) == 1 ? L.tab : a.tab16;  // the uint8 table is filled lazily (first exact replay)
   uint32_t phase = 0;
   if (a.plan.use_tma && threadIdx.x == 0) mbar_init(L.bar, 1);
-  StageResult res;
-  for (int attempt = 0;; ++attempt) {  // no valid candidate: re-centre on (0, 0) (fme.py:310-313)
-    res = stage_search<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox, oy, b, attempt ? 0 : sx,
-                                            attempt ? 0 : sy, a.r, a.s);
-    if (res.nvalid || attempt) break;
-  }
-  if (threadIdx.x != 0) return;
-  if (a.single) {
-    a.mv[0] = res.dx;
-    a.mv[1] = res.dy;
-    a.energy[0] = res.energy;
-    a.nvalid_out[0] = res.nvalid;
-    return;
-  }
-  a.mv[2 * cell] = res.dx;
-  a.mv[2 * cell + 1] = res.dy;
-  a.energy[cell] = res.energy;
-  if (a.last) {
-    bool m;
-    if (a.final_level) {
-      const bool in_real = oy < p.real_h && ox < p.real_w;  // fme.py:377-384
-      m = !(res.energy > p.refine_block_threshold && in_real);
+  // Persistent CTAs: the grid is sized to the resident capacity and strides
+  // over the (pair, block) work list, so the prologue and the per-stage
+  // constants are paid once per CTA, not once per block.
+  const uint32_t cells = (uint32_t)a.gw * a.gh;
+  const uint32_t total = a.single ? 1u : cells * (uint32_t)a.n_pairs;
+  for (uint32_t work = blockIdx.x; work < total; work += gridDim.x) {
+    int pair = 0, gx = 0, gy = 0, ox, oy, sx = 0, sy = 0;
+    long long cell = 0;
+    if (a.single) {
+      ox = a.ox;
+      oy = a.oy;
+      sx = a.cx;
+      sy = a.cy;
     } else {
-      m = res.energy <= p.split_threshold;  // fme.py:386
+      pair = (int)(work / cells);
+      const int blk = (int)(work - (uint32_t)pair * cells);
+      gx = blk % a.gw;
+      gy = blk / a.gw;
+      cell = (long long)pair * cells + blk;
+      ox = gx * b;
+      oy = gy * b;
+      if (a.level > 0) {
+        const int pgw = a.gw / 2, pgh = a.gh / 2;
+        const long long pcell = (long long)pair * pgw * pgh + (gy / 2) * pgw + (gx / 2);
+        if (a.parent_matched[pcell]) {  // inherited: copy the parent (fme.py:352-362)
+          if (a.first && threadIdx.x == 0) {
+            a.mv[2 * cell] = a.parent_mv[2 * pcell];
+            a.mv[2 * cell + 1] = a.parent_mv[2 * pcell + 1];
+            a.energy[cell] = a.parent_e[pcell];
+            a.matched[cell] = 1;
+          }
+          continue;
+        }
+        if (a.first) {
+          sx = a.parent_mv[2 * pcell];
+          sy = a.parent_mv[2 * pcell + 1];
+        }
+      }
+      if (!a.first) {
+        sx = a.mv[2 * cell];
+        sy = a.mv[2 * cell + 1];
+      }
     }
-    a.matched[cell] = m ? 1 : 0;
+    PairCtx<Elem> pc;
+    const int cur_f = a.single ? 0 : a.cur_index[pair];
+    const int ref_f = a.single ? 0 : a.ref_index[pair];
+    pc.cur = reinterpret_cast<const Elem*>(a.planes) + (long long)cur_f * p.frame_stride;
+    pc.ref = reinterpret_cast<const Elem*>(a.ref_planes) + (long long)ref_f * p.frame_stride;
+    pc.cur_z = cur_f * p.planes;
+    pc.ref_z = ref_f * p.planes;
+    pc.pitch = p.pitch;
+    pc.plane_stride = p.plane_stride;
+    pc.frame_h = a.single ? p.real_h : p.pad_h;  // search_stage works on unpadded planes (fme.py:279-284)
+    pc.frame_w = a.single ? p.real_w : p.pad_w;
+    pc.P = p.planes;
+    pc.max_value = p.max_value;
+    pc.tol = p.sparsity_tolerance;
+    pc.lam = p.lam;
+    pc.oml = p.one_minus_lam;
+    pc.tab = sizeof(Elem) == 1 ? L.tab : a.tab16;  // the uint8 table is filled lazily (first exact replay)
+    StageResult res;
+    for (int attempt = 0;; ++attempt) {  // no valid candidate: re-centre on (0, 0) (fme.py:310-313)
+      res = stage_search<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox, oy, b, attempt ? 0 : sx,
+                                              attempt ? 0 : sy, a.r, a.s);
+      if (res.nvalid || attempt) break;
+    }
+    if (threadIdx.x != 0) continue;
+    if (a.single) {
+      a.mv[0] = res.dx;
+      a.mv[1] = res.dy;
+      a.energy[0] = res.energy;
+      a.nvalid_out[0] = res.nvalid;
+      continue;
+    }
+    a.mv[2 * cell] = res.dx;
+    a.mv[2 * cell + 1] = res.dy;
+    a.energy[cell] = res.energy;
+    if (a.last) {
+      bool m;
+      if (a.final_level) {
+        const bool in_real = oy < p.real_h && ox < p.real_w;  // fme.py:377-384
+        m = !(res.energy > p.refine_block_threshold && in_real);
+      } else {
+        m = res.energy <= p.split_threshold;  // fme.py:386
+      }
+      a.matched[cell] = m ? 1 : 0;
+    }
+    atomicAdd(a.evals + pair, (unsigned long long)(res.nvalid + a.extra_evals));
   }
-  atomicAdd(a.evals + pair, (unsigned long long)(res.nvalid + a.extra_evals));
 }
 
 template <typename K>
@@ -819,7 +841,46 @@ inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageL
             "pg %d tma %d box %dx%d copies %d smem %d\n", (int)sizeof(E), CW, TY, (int)SH, a.level, a.b, a.r, a.s,
             grid.x, grid.y, a.plan.threads, a.plan.parts, a.plan.pg, a.plan.use_tma, a.plan.bw, a.plan.hwin,
             a.plan.copies, a.plan.smem);
-  fme_stage_kernel<E, CW, TY, SH><<<grid, a.plan.threads, a.plan.smem, st>>>(tw, tc, a);
+  // persistent grid: resident capacity (occupancy x SMs), capped by the work count
+  static std::mutex omu;
+  static const void* okeys[512];
+  static int othreads[512], osmem[512], ovals[512];
+  static int on = 0;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> g(omu);
+    const void* key = reinterpret_cast<const void*>(fme_stage_kernel<E, CW, TY, SH>);
+    for (int i = 0; i < on; ++i)
+      if (okeys[i] == key && othreads[i] == a.plan.threads && osmem[i] == a.plan.smem) per_sm = ovals[i];
+    if (!per_sm) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fme_stage_kernel<E, CW, TY, SH>,
+                                                                    a.plan.threads, a.plan.smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      if (per_sm < 1) per_sm = 1;
+      if (on < 512) {
+        okeys[on] = key;
+        othreads[on] = a.plan.threads;
+        osmem[on] = a.plan.smem;
+        ovals[on] = per_sm;
+        ++on;
+      }
+    }
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+  }
+  const long long work = (long long)grid.x * grid.y;
+  static const int persist_mult = [] {  // resident waves per launch; 0 = one CTA per block
+    const char* e = getenv("BMC_PERSIST");
+    return e ? atoi(e) : 0;
+  }();
+  const long long capacity = persist_mult > 0 ? (long long)per_sm * sms * persist_mult : work;
+  const unsigned nblk = (unsigned)(work < capacity ? work : capacity);
+  fme_stage_kernel<E, CW, TY, SH><<<nblk, a.plan.threads, a.plan.smem, st>>>(tw, tc, a);
   rc = cuda_status(cudaGetLastError(), "fme_stage_kernel");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (!rc && sync_debug() && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {

@@ -39,7 +39,7 @@ struct StageLaunch {
   StagePlan plan;
   const int32_t* cur_index;
   const int32_t* ref_index;
-  int level, final_level, b, gw, gh;
+  int level, final_level, b, gw, gh, n_pairs;
   int first, last;          // first / last searched stage of the level
   int r, s;
   int extra_evals;          // range-0 stages folded into this launch's candidate count
@@ -106,6 +106,8 @@ int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p
 int launch_refine(const RefineArgs& a, cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);
 int launch_predict(const PredictArgs& a, int n_streams, cudaStream_t st);
+int launch_predict_chain(const PredictArgs& a, int n_streams, int t_begin, int t_end, unsigned* barrier_ctr,
+                         cudaStream_t st);
 int launch_predict_features(const float* src, float* dst, int C, int H, int W, const int32_t* mv, int gw, int B,
                             int scale, cudaStream_t st);
 int launch_block_energy(const double* a, const double* b, long long n, double lam, double tol, double* out,

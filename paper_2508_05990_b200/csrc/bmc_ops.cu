@@ -268,8 +268,120 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const DecideArgs a) {
   }
 }
 
+// Register-resident AEM scan for the "max" statistic (the common case): each
+// thread owns up to kDecideCells coarse cells for the whole clip; the pooled
+// energies of frame t+1 are loaded while frame t is reduced, so a frame costs
+// one CTA max-reduction and two barriers instead of global round trips.
+// Operation order per cell is the reference's: acc' = acc + pooled (float64),
+// trigger = max over cells (exact), key resets acc to 0 (frame_select.py:99-136).
+constexpr int kDecideThreads = 1024;
+constexpr int kDecideCells = 4;
+
+__device__ __forceinline__ double pooled_cell(const double* __restrict__ e, int c, const bmc_select_params& sp) {
+  if (sp.factor == 1) return e[c];
+  const int cy = c / sp.coarse_w, cx = c - cy * sp.coarse_w;
+  double v = -INFINITY;
+  for (int dy = 0; dy < sp.factor; ++dy)
+    for (int dx = 0; dx < sp.factor; ++dx) v = fmax(v, e[(cy * sp.factor + dy) * sp.grid_w + cx * sp.factor + dx]);
+  return v;
+}
+
+__global__ void __launch_bounds__(kDecideThreads) decide_max_kernel(const DecideArgs a) {
+  __shared__ double red[kDecideThreads / 32];
+  __shared__ int is_key_s;
+  const int stream = blockIdx.x;
+  const bmc_select_params& sp = a.sp;
+  const int ncoarse = sp.coarse_h * sp.coarse_w;
+  double* accg = a.acc + (long long)stream * ncoarse;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[kDecideCells], nxt[kDecideCells];
+#pragma unroll
+  for (int k = 0; k < kDecideCells; ++k) {
+    const int c = threadIdx.x + k * kDecideThreads;
+    acc[k] = c < ncoarse ? accg[c] : 0.0;
+    nxt[k] = 0.0;
+  }
+  auto load_frame = [&](int t, double (&dst)[kDecideCells]) {
+    const double* e = a.energy + stream * a.ess + t * a.efs;
+#pragma unroll
+    for (int k = 0; k < kDecideCells; ++k) {
+      const int c = threadIdx.x + k * kDecideThreads;
+      dst[k] = c < ncoarse ? pooled_cell(e, c, sp) : 0.0;
+    }
+  };
+  load_frame(a.t_begin, nxt);
+  int fsk = a.fsk[stream], last_key = a.last_key[stream];
+  for (int t = a.t_begin; t < a.t_end; ++t) {
+    double cur[kDecideCells];
+#pragma unroll
+    for (int k = 0; k < kDecideCells; ++k) cur[k] = nxt[k];
+    if (t + 1 < a.t_end) load_frame(t + 1, nxt);  // prefetch: independent of the scan state
+    double mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kDecideCells; ++k) {
+      const int c = threadIdx.x + k * kDecideThreads;
+      if (c < ncoarse) {
+        acc[k] = __dadd_rn(acc[k], cur[k]);
+        mx = fmax(mx, acc[k]);
+      }
+    }
+    for (int m = 16; m; m >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (warp == 0) {
+      double r = lane < (int)(blockDim.x >> 5) ? red[lane] : -INFINITY;
+      for (int m = 16; m; m >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, m));
+      if (lane == 0) {
+        const int f = fsk + 1;
+        const bool key = r > sp.aem_threshold || (sp.has_max_gop && f >= sp.max_gop);
+        int kind, ref;
+        if (key) {
+          kind = 0;
+          ref = -1;
+          fsk = 0;
+          last_key = t;
+        } else if (sp.policy_keyframe) {
+          kind = 2;
+          ref = last_key;
+          fsk = f;
+        } else {
+          kind = 1;
+          ref = t - 1;
+          fsk = f;
+        }
+        const long long o = (long long)stream * a.dss + t;
+        a.kind[o] = kind;
+        a.ref[o] = ref;
+        a.trigger[o] = r;
+        if (a.ref_next)
+          a.ref_next[stream] = stream * a.frames_per_stream + (sp.policy_keyframe ? last_key : t);
+        is_key_s = key;
+      }
+    }
+    __syncthreads();
+    if (is_key_s) {
+#pragma unroll
+      for (int k = 0; k < kDecideCells; ++k) acc[k] = 0.0;
+    }
+    // red[] and is_key_s are rewritten only after the next frame's first barrier
+  }
+#pragma unroll
+  for (int k = 0; k < kDecideCells; ++k) {
+    const int c = threadIdx.x + k * kDecideThreads;
+    if (c < ncoarse) accg[c] = acc[k];
+  }
+  if (threadIdx.x == 0) {
+    a.fsk[stream] = fsk;
+    a.last_key[stream] = last_key;
+  }
+}
+
 int launch_decide(const DecideArgs& a, cudaStream_t st) {
   const int ncoarse = a.sp.coarse_h * a.sp.coarse_w;
+  if (!a.sp.statistic_mean && ncoarse <= kDecideThreads * kDecideCells) {
+    decide_max_kernel<<<a.n_streams, kDecideThreads, 0, st>>>(a);
+    return cuda_status(cudaGetLastError(), "decide_max_kernel");
+  }
   const long long nleaf = pairwise_leaf_count(ncoarse);
   const size_t smem = (size_t)nleaf * (8 + 8 + 4) + 16;
   if (smem > 200 * 1024) {
@@ -345,6 +457,131 @@ int launch_predict(const PredictArgs& a, int n_streams, cudaStream_t st) {
   if (bx < 1) bx = 1;
   predict_kernel<<<dim3((unsigned)bx, n_streams), kThreads, 0, st>>>(a);
   return cuda_status(cudaGetLastError(), "predict_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Whole-clip label chain in ONE cooperative launch: frames are processed in
+// order (frame t's reference labels are frame t-1's or the last key's output,
+// both earlier), separated by a grid-wide barrier; every CTA strides over the
+// (stream, row, 16-byte group) tasks of the frame.  Key frames copy their
+// injected labels with 16-byte loads/stores; other frames gather, with a
+// 5-word funnel-shift fast path when the 16 pixels share one block and need no
+// clamping (propagate.py:39-53 semantics either way).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (*((volatile unsigned*)ctr) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictArgs a, int n_streams, int t_begin,
+                                                                 int t_end, unsigned* barrier_ctr) {
+  const int groups_per_row = (a.W + 15) / 16;
+  const long long per_stream = (long long)a.H * groups_per_row;
+  const long long total = per_stream * n_streams;
+  const bool vec_ok = (a.W % 16 == 0) && (a.fs % 16 == 0) && (a.ss % 16 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(a.labels) & 15) == 0) &&
+                      (!a.key_labels || (reinterpret_cast<uintptr_t>(a.key_labels) & 15) == 0);
+  unsigned epoch = 0;
+  for (int t = t_begin; t < t_end; ++t) {
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+         g += (long long)gridDim.x * blockDim.x) {
+      const int stream = (int)(g / per_stream);
+      const long long gg = g - stream * per_stream;
+      const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
+      const long long o = (long long)stream * a.kss + t;
+      const int kind = a.kind ? a.kind[o] : 1;
+      uint8_t* out = a.labels + stream * a.ss + t * a.fs + (long long)y * a.W;
+      const int n = min(16, a.W - x0);
+      if (kind == 0) {
+        const uint8_t* src = a.key_labels + stream * a.ss + t * a.fs + (long long)y * a.W;
+        if (vec_ok) {
+          *reinterpret_cast<uint4*>(out + x0) = __ldcs(reinterpret_cast<const uint4*>(src + x0));
+        } else {
+          for (int e = 0; e < n; ++e) out[x0 + e] = src[x0 + e];
+        }
+        continue;
+      }
+      const int r = a.ref ? a.ref[o] : a.ref_fixed;
+      const uint8_t* src = a.labels + stream * a.ss + (long long)r * a.fs;
+      const int32_t* mv = a.mv + stream * a.mvss + t * a.mvfs;
+      const int gy = y / a.B;
+      const int gx0 = x0 / a.B, gx1 = (x0 + n - 1) / a.B;
+      if (vec_ok && n == 16 && gx0 == gx1) {
+        const int c = gy * a.gw + gx0;
+        const int dx = __ldg(mv + 2 * c) * a.scale, dy = __ldg(mv + 2 * c + 1) * a.scale;
+        const int sy = min(max(y + dy, 0), a.H - 1);
+        const int sx = x0 + dx;
+        if (sx >= 0 && sx + 16 <= a.W) {
+          const uint32_t* row = reinterpret_cast<const uint32_t*>(src + (long long)sy * a.W);
+          const int w0 = sx >> 2, sh = (sx & 3) * 8;
+          uint32_t v[5];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = __ldcg(row + w0 + q);
+          v[4] = sh ? __ldcg(row + w0 + 4) : 0u;
+          uint4 o4;
+          o4.x = __funnelshift_r(v[0], v[1], sh);
+          o4.y = __funnelshift_r(v[1], v[2], sh);
+          o4.z = __funnelshift_r(v[2], v[3], sh);
+          o4.w = __funnelshift_r(v[3], v[4], sh);
+          *reinterpret_cast<uint4*>(out + x0) = o4;
+          continue;
+        }
+      }
+      uint32_t words[4] = {0, 0, 0, 0};
+      int gxc = -1, dx = 0, sy = 0;
+      for (int e = 0; e < n; ++e) {
+        const int x = x0 + e;
+        const int gx = x / a.B;
+        if (gx != gxc) {
+          gxc = gx;
+          const int c = gy * a.gw + gx;
+          dx = __ldg(mv + 2 * c) * a.scale;
+          const int dy = __ldg(mv + 2 * c + 1) * a.scale;
+          sy = min(max(y + dy, 0), a.H - 1);
+        }
+        const int sx = min(max(x + dx, 0), a.W - 1);
+        words[e >> 2] |= (uint32_t)__ldcg(src + (long long)sy * a.W + sx) << (8 * (e & 3));
+      }
+      if (vec_ok && n == 16) {
+        *reinterpret_cast<uint4*>(out + x0) = make_uint4(words[0], words[1], words[2], words[3]);
+      } else {
+        for (int e = 0; e < n; ++e) out[x0 + e] = (uint8_t)(words[e >> 2] >> (8 * (e & 3)));
+      }
+    }
+    if (t + 1 < t_end) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
+  }
+}
+
+int launch_predict_chain(const PredictArgs& a, int n_streams, int t_begin, int t_end, unsigned* barrier_ctr,
+                         cudaStream_t st) {
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_chain_kernel, kThreads, 0);
+    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(predict)");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long tasks = (long long)n_streams * a.H * ((a.W + 15) / 16);
+  long long grid = (tasks + kThreads - 1) / kThreads;
+  const long long cap = (long long)per_sm * sms;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  int rc = cuda_status(cudaMemsetAsync(barrier_ctr, 0, sizeof(unsigned), st), "memset predict barrier");
+  if (rc) return rc;
+  PredictArgs a2 = a;
+  void* args[] = {(void*)&a2, (void*)&n_streams, (void*)&t_begin, (void*)&t_end, (void*)&barrier_ctr};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)predict_chain_kernel, dim3((unsigned)grid), dim3(kThreads),
+                                              args, 0, st);
+  return cuda_status(e, "predict_chain_kernel");
 }
 
 __global__ void predict_features_kernel(const float* __restrict__ src, float* __restrict__ dst, int C, int H, int W,

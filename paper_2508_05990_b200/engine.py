@@ -7,7 +7,7 @@ This is the B200 replacement of the per-frame loop in ``run_sequence``
   ME for every frame pair, all levels              bmc_estimate_motion
   3x3 MV refinement + energy re-evaluation         bmc_refine_mvs
   AEM key-frame scan over the clip                 bmc_decide
-  label propagation chain (key copy / gather)      bmc_predict_labels x T
+  label propagation chain (key copy / gather)      bmc_predict_labels_clip (one cooperative launch)
 
 all enqueued on one CUDA stream with no host synchronisation, so the whole
 step can be captured in a CUDA graph.  With the default "previous" reference
@@ -86,6 +86,7 @@ class ClipEngine:
         self.kind = torch.zeros((S, T), dtype=torch.int32, device=self.dev)
         self.ref = torch.full((S, T), -1, dtype=torch.int32, device=self.dev)
         self.trigger = torch.zeros((S, T), dtype=torch.float64, device=self.dev)
+        self.workspace = torch.zeros(4, dtype=torch.int32, device=self.dev)  # label-chain grid barrier
         self.set_label_size(*(label_hw or (self.H, self.W)))
         self.graph = None
 
@@ -168,16 +169,15 @@ class ClipEngine:
             N.ptr(self.e_ref[lo:hi]), N.ptr(self.replaced[lo:hi]), N.stream_handle()))
 
     def predict(self) -> None:
-        """Label chain: key frames copy key_labels, others gather from their reference."""
+        """Label chain (one cooperative launch): key frames copy key_labels, others gather from their reference."""
         lib = N.load()
         st = N.stream_handle()
         cells2 = self.gh * self.gw * 2
         fs = self.Hl * self.Wl
-        for t in range(self.T):
-            N.check(lib.bmc_predict_labels(
-                N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, t, N.ptr(self.kind),
-                N.ptr(self.ref), 0, self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
-                self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale, st))
+        N.check(lib.bmc_predict_labels_clip(
+            N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, 0, self.T, N.ptr(self.kind),
+            N.ptr(self.ref), self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
+            self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale, N.ptr(self.workspace), st))
 
     def step(self) -> None:
         self.motion()
