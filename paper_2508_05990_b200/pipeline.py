@@ -17,10 +17,12 @@ component on the roadmap and is not part of this build, so
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native as N
 from .config import PipelineConfig
 from .engine import ClipEngine
 from .fme import count_fme_flops, mv_scale
@@ -141,14 +143,26 @@ class ClipSession:
     ``run(raw, key_labels)`` takes a (T, H, W) uint8/uint16 Bayer (or luma)
     clip in host memory, runs ME -> refine -> decide -> predict on the GPU and
     returns ``(labels (T, Hl, Wl) uint8 ndarray, kinds, refs, triggers)``.
-    ``key_labels`` is a callable / mapping frame -> LabelMap consulted exactly
-    once per key frame, as in ``run_sequence``.  Device buffers and pinned
-    staging buffers are allocated once per session, so repeated clips of the
-    same geometry pay only the transfers and the kernels.
+
+    ``key_labels`` is either
+      * a callable / mapping frame -> LabelMap consulted exactly once per key
+        frame, in frame order, as ``run_sequence`` does (decisions are read back
+        first, then the key frames' labels are uploaded), or
+      * a (T, Hl, Wl) uint8 tensor (pinned for full speed) holding a label map
+        for every frame; only the key frames' maps are used (reference
+        semantics), and the upload overlaps motion estimation.
+
+    With the default "previous" reference policy the clip is processed in
+    ``chunks`` frame ranges on three streams: the H2D copy of chunk c+1
+    overlaps pack + ME of chunk c; refine and the AEM scan follow; the label
+    chain then runs per chunk with each chunk's D2H overlapping the next
+    chunk's gathers.  Results are identical to ``run_sequence`` (the chunking
+    only changes launch boundaries).  The returned label array is owned by the
+    session and overwritten by the next ``run``.
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True):
+                 bayer: bool = True, chunks: int = 3):
         if config.refine_enabled:
             raise NotImplementedError("CaBR-Net block refinement is not part of the B200 hot path yet; "
                                       "run with PipelineConfig(refine_enabled=False)")
@@ -158,22 +172,20 @@ class ClipSession:
         self.pin_raw = torch.empty(tuple(self.eng.raw.shape[1:]), dtype=self.eng.raw.dtype).pin_memory()
         self.pin_labels = torch.empty(tuple(self.eng.labels.shape[1:]), dtype=torch.uint8).pin_memory()
         self.pin_key = torch.empty(tuple(self.eng.labels.shape[1:]), dtype=torch.uint8).pin_memory()
+        self.pin_dec = torch.empty((3, n_frames), dtype=torch.float64).pin_memory()
+        self.copy_in = torch.cuda.Stream()
+        self.copy_out = torch.cuda.Stream()
+        t = int(n_frames)
+        k = max(1, min(int(chunks), t))
+        bounds = [round(i * t / k) for i in range(k + 1)]
+        self.chunks = [(bounds[i], bounds[i + 1]) for i in range(k) if bounds[i + 1] > bounds[i]]
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
-    def run(self, raw, key_labels):
+    # -- helpers ----------------------------------------------------------------
+    def _lookup_keys(self, lookup, kinds):
         eng, torch = self.eng, self.torch
-        lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
-        src = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(raw))
-        if src.is_pinned():
-            eng.raw[0].copy_(src, non_blocking=True)
-        else:
-            self.pin_raw.copy_(src)
-            eng.raw[0].copy_(self.pin_raw, non_blocking=True)
-        h2d = src.numel() * src.element_size()
-        eng.motion()
-        kinds, refs, trig = (a[0] for a in eng.decisions_host())
-        d2h = kinds.nbytes + refs.nbytes + trig.nbytes
+        h2d = 0
         for i in np.nonzero(kinds == 0)[0].tolist():
             try:
                 lab = lookup(i)
@@ -183,12 +195,90 @@ class ClipSession:
                 raise MissingKeyLabels(i)
             if (lab.height, lab.width) != (eng.Hl, eng.Wl):
                 raise ValueError("key label maps must match the session's label size")
-            self.pin_key[i].copy_(torch.from_numpy(np.array(lab.classes)))
+            np.copyto(self.pin_key[i].numpy(), lab.classes)
             eng.key_labels[0, i].copy_(self.pin_key[i], non_blocking=True)
             h2d += lab.classes.nbytes
-        eng.predict()
-        self.pin_labels.copy_(eng.labels[0], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        return h2d
+
+    def run(self, raw, key_labels):
+        eng, torch = self.eng, self.torch
+        lib = N.load()
+        cs = torch.cuda.current_stream()
+        st = N.stream_handle(cs)
+        src = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(raw))
+        if not src.is_pinned():
+            self.pin_raw.copy_(src)
+            src = self.pin_raw
+        label_tensor = key_labels if isinstance(key_labels, torch.Tensor) else None
+        lookup = None
+        if label_tensor is None:
+            lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
+        elif tuple(label_tensor.shape) != tuple(eng.labels.shape[1:]):
+            raise ValueError(f"key label tensor must be {tuple(eng.labels.shape[1:])}, got {tuple(label_tensor.shape)}")
+        h2d = src.numel() * src.element_size()
+        p = eng.params
+        fstride = p.frame_stride
+        esz = eng.planes.element_size()
+        eng._reset_state()
+        pipelined = eng.cfg.reference_policy == "previous" and eng.T >= 2
+        if pipelined:
+            for f0, f1 in self.chunks:
+                ev = torch.cuda.Event()
+                with torch.cuda.stream(self.copy_in):
+                    self.copy_in.wait_stream(cs)  # previous users of eng.raw are done
+                    eng.raw[0, f0:f1].copy_(src[f0:f1], non_blocking=True)
+                    ev.record(self.copy_in)
+                cs.wait_event(ev)
+                N.check(lib.bmc_pack_planes(N.ptr(eng.raw[0, f0]), f1 - f0, eng.kind_code, ctypes.byref(p),
+                                            N.ptr(eng.planes) + f0 * fstride * esz, st))
+                p0, p1 = max(f0, 1) - 1, f1 - 1  # pairs whose frames are resident: t in [max(f0,1), f1)
+                if p1 > p0:
+                    arr = eng._level_slice(p0, p1)
+                    N.check(lib.bmc_estimate_motion(N.ptr(eng.planes), eng.S * eng.T, ctypes.byref(p), p1 - p0,
+                                                    N.ptr(eng.cur_index[p0:p1]), N.ptr(eng.ref_index[p0:p1]), arr, st))
+            if label_tensor is not None:
+                ev_lab = torch.cuda.Event()
+                with torch.cuda.stream(self.copy_in):
+                    eng.key_labels[0].copy_(label_tensor, non_blocking=True)
+                    ev_lab.record(self.copy_in)
+            eng._refine(0, eng.n_pairs)
+            eng._decide(1, eng.T)
+        else:
+            eng.raw[0].copy_(src, non_blocking=True)
+            eng.motion()
+            if label_tensor is not None:
+                eng.key_labels[0].copy_(label_tensor, non_blocking=True)
+        dec = torch.stack([eng.kind[0].double(), eng.ref[0].double(), eng.trigger[0]])
+        d2h = self.pin_dec.numel() * 8  # kind, ref, trigger (float64 rows)
+        if label_tensor is None:
+            self.pin_dec.copy_(dec)  # synchronous: the key lookups need the decisions
+            kinds = self.pin_dec[0].numpy().astype(np.int32)
+            h2d += self._lookup_keys(lookup, kinds)
+        else:
+            if pipelined:
+                cs.wait_event(ev_lab)
+            h2d += label_tensor.numel()  # whole tensor uploaded (every frame's map is an input)
+        # label chain per chunk; each chunk's D2H overlaps the next chunk's gathers
+        cells2 = eng.gh * eng.gw * 2
+        fs = eng.Hl * eng.Wl
+        chunks = self.chunks if pipelined else [(0, eng.T)]
+        for f0, f1 in chunks:
+            N.check(lib.bmc_predict_labels_clip(
+                N.ptr(eng.labels), fs, eng.T * fs, N.ptr(eng.key_labels), eng.S, f0, f1, N.ptr(eng.kind),
+                N.ptr(eng.ref), eng.T, eng.Hl, eng.Wl, N.ptr(eng.mv_ref) - 4 * eng.S * cells2,
+                eng.S * cells2, cells2, eng.gh, eng.gw, eng.b_final, eng.scale, N.ptr(eng.workspace), st))
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            with torch.cuda.stream(self.copy_out):
+                self.copy_out.wait_event(ev)
+                self.pin_labels[f0:f1].copy_(eng.labels[0, f0:f1], non_blocking=True)
+        if label_tensor is not None:
+            with torch.cuda.stream(self.copy_out):
+                self.pin_dec.copy_(dec, non_blocking=True)
+        self.copy_out.synchronize()
+        kinds = self.pin_dec[0].numpy().astype(np.int32)
+        refs = self.pin_dec[1].numpy().astype(np.int32)
+        trig = self.pin_dec[2].numpy().copy()
         d2h += self.pin_labels.numel()
         self.h2d_bytes, self.d2h_bytes = h2d, d2h
         return self.pin_labels.numpy(), kinds, refs, trig

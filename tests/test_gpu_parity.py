@@ -361,3 +361,38 @@ def test_clip_engine_multistream(cuda):
         got = eng.labels[s].cpu().numpy()
         for t in range(T):
             np.testing.assert_array_equal(got[t], olab[t])
+
+
+@pytest.mark.parametrize("variant", ["callable", "tensor", "gop3", "keyframe"])
+def test_clip_session_matches_run_sequence(cuda, variant):
+    """The pipelined host-buffer session (chunked H2D / ME / label chain / D2H on three
+    streams) returns exactly what run_sequence returns, for both key-label forms."""
+    from paper_2508_05990_b200 import synth
+    from paper_2508_05990_b200.config import PipelineConfig
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    from paper_2508_05990_b200.pipeline import ClipSession, run_sequence
+    w, h, t = 192, 128, 11
+    clip = synth.bayer_pan_clip(w, h, t, (4, -2), seed=21, square=32, square_velocity=(5, 3))
+    labels = synth.block_labels(w, h, t, seed=4)
+    fcfg = FmeConfig(stages=(SearchStage(4, 1), SearchStage(0, 1), SearchStage(1, 1)), block_sizes=(16,))
+    kw = dict(fme=fcfg, refine_enabled=False, aem_threshold=0.02)
+    if variant == "gop3":
+        kw.update(max_gop=3, aem_threshold=float("inf"))
+    if variant == "keyframe":
+        kw.update(reference_policy="keyframe")
+    pcfg = PipelineConfig(**kw)
+    ref = run_sequence(synth.frames_of(clip), labels, pcfg)
+    sess = ClipSession(pcfg, h, w, t, np.uint8, True, chunks=3)
+    if variant == "tensor":
+        key = cuda.from_numpy(np.stack([l.classes for l in labels])).pin_memory()
+    else:
+        key = {i: labels[i] for i in range(t)}
+    for _ in range(2):  # a second run on the same session must not see stale state
+        got, kinds, refs, trig = sess.run(cuda.from_numpy(clip).pin_memory(), key)
+        for i, d in enumerate(ref.decisions):
+            assert ("key", "nonkey_prev_ref", "nonkey_key_ref")[kinds[i]] == d.kind.value
+            assert trig[i] == d.trigger_statistic
+            if kinds[i] != 0:
+                assert refs[i] == d.reference_index
+        for i in range(t):
+            np.testing.assert_array_equal(got[i], ref.labels[i].classes)
