@@ -16,54 +16,93 @@ namespace bmc {
 // [pad_w, pitch) are filled the same way so staging may read whole words.
 // ---------------------------------------------------------------------------
 template <typename Elem>
-__global__ void pack_kernel(const Elem* __restrict__ raw, long long n_words, int kind, int H, int W,
-                            const bmc_fme_params p, Elem* __restrict__ planes) {
+__device__ __forceinline__ uint32_t pack_pick(const Elem* __restrict__ row, int x0, int step, int w, int real_w) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  uint32_t word = 0;
+#pragma unroll
+  for (int e = 0; e < EPW; ++e) {
+    const int xs = min(w * EPW + e, real_w - 1);
+    word |= (uint32_t)__ldg(row + x0 + step * xs) << (8 * sizeof(Elem) * e);
+  }
+  return word;
+}
+
+// One thread turns 8 raw bytes of one raw row into one 32-bit word of each of
+// the two CFA planes that row feeds (even / odd columns, split with PRMT), so
+// reads and writes are both coalesced 8- / 4-byte accesses.  blockIdx.y walks
+// (frame, plane row, raw-row parity); words that touch the right padding take
+// the clamped per-sample path.
+template <typename Elem>
+__global__ void pack_kernel(const Elem* __restrict__ raw, int kind, int H, int W, const bmc_fme_params p,
+                            Elem* __restrict__ planes) {
   constexpr int EPW = 4 / sizeof(Elem);
   const int wpr = p.pitch / EPW;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n_words;
-       idx += (long long)gridDim.x * blockDim.x) {
-    long long t = idx;
-    const int w = (int)(t % wpr);
-    t /= wpr;
-    const int y = (int)(t % p.pad_h);
-    t /= p.pad_h;
-    const int pl = (int)(t % p.planes);
-    const long long f = t / p.planes;
-    const int ys = min(y, p.real_h - 1);
-    const Elem* src;
-    int step, x0;
-    if (kind == BMC_KIND_BAYER) {
-      src = raw + f * H * (long long)W + (long long)(2 * ys + (pl >> 1)) * W;
-      step = 2;
-      x0 = pl & 1;
+  const bool bayer = kind == BMC_KIND_BAYER;
+  const int par = bayer ? 2 : 1;
+  const int rowsel = blockIdx.y;  // (f * pad_h + y) * par + parity
+  const int parity = bayer ? (rowsel & 1) : 0;
+  const int fy = bayer ? (rowsel >> 1) : rowsel;
+  const int f = fy / p.pad_h, y = fy - f * p.pad_h;
+  const int ys = min(y, p.real_h - 1);
+  const Elem* frame = raw + (long long)f * H * W;
+  Elem* out = planes + (long long)f * p.frame_stride + (long long)y * p.pitch;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < wpr; w += gridDim.x * blockDim.x) {
+    if (!bayer) {
+      const Elem* row = frame + (long long)ys * W;
+      const uint32_t word = ((w + 1) * EPW <= p.real_w && (W % EPW) == 0)
+                                ? __ldg(reinterpret_cast<const uint32_t*>(row) + w)
+                                : pack_pick<Elem>(row, 0, 1, w, p.real_w);
+      reinterpret_cast<uint32_t*>(out)[w] = word;
+      continue;
+    }
+    const Elem* row = frame + (long long)(2 * ys + parity) * W;
+    uint32_t ev, od;
+    if ((w + 1) * EPW <= p.real_w && (W % (2 * EPW)) == 0) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(row) + w);  // 2*EPW raw samples
+      if constexpr (EPW == 4) {
+        ev = __byte_perm(v.x, v.y, 0x6420);
+        od = __byte_perm(v.x, v.y, 0x7531);
+      } else {
+        ev = __byte_perm(v.x, v.y, 0x5410);
+        od = __byte_perm(v.x, v.y, 0x7632);
+      }
     } else {
-      src = raw + f * H * (long long)W + (long long)ys * W;
-      step = 1;
-      x0 = 0;
+      ev = pack_pick<Elem>(row, 0, 2, w, p.real_w);
+      od = pack_pick<Elem>(row, 1, 2, w, p.real_w);
     }
-    uint32_t word = 0;
-#pragma unroll
-    for (int e = 0; e < EPW; ++e) {
-      const int xs = min(w * EPW + e, p.real_w - 1);
-      word |= (uint32_t)__ldg(src + x0 + step * xs) << (8 * sizeof(Elem) * e);
-    }
-    reinterpret_cast<uint32_t*>(planes + f * p.frame_stride + pl * p.plane_stride + (long long)y * p.pitch)[w] = word;
+    reinterpret_cast<uint32_t*>(out + (2 * parity) * p.plane_stride)[w] = ev;
+    reinterpret_cast<uint32_t*>(out + (2 * parity + 1) * p.plane_stride)[w] = od;
   }
 }
 
 int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p, void* planes, cudaStream_t st) {
   const int epw = 4 / p.elem_bytes;
-  const long long n_words = (long long)n_frames * p.planes * p.pad_h * (p.pitch / epw);
-  const int blocks = (int)((n_words + kThreads - 1) / kThreads < 148 * 16 ? (n_words + kThreads - 1) / kThreads
-                                                                          : 148 * 16);
+  const int wpr = p.pitch / epw;
+  const int par = kind == BMC_KIND_BAYER ? 2 : 1;
+  const int rows_per_frame = p.pad_h * par;
+  if (rows_per_frame > 65535) {
+    set_error("frame too tall for the pack kernel");
+    return BMC_E_ARG;
+  }
   const int H = p.planes == 4 ? p.real_h * 2 : p.real_h;
   const int W = p.planes == 4 ? p.real_w * 2 : p.real_w;
-  if (p.elem_bytes == 1)
-    pack_kernel<uint8_t><<<blocks, kThreads, 0, st>>>((const uint8_t*)raw, n_words, kind, H, W, p, (uint8_t*)planes);
-  else
-    pack_kernel<uint16_t><<<blocks, kThreads, 0, st>>>((const uint16_t*)raw, n_words, kind, H, W, p,
-                                                       (uint16_t*)planes);
-  return cuda_status(cudaGetLastError(), "pack_kernel");
+  const int tpb = 128;
+  const unsigned gx = (unsigned)((wpr + tpb - 1) / tpb);
+  const int frames_per_launch = 65535 / rows_per_frame;  // grid.y limit
+  const size_t eb = p.elem_bytes;
+  for (int f0 = 0; f0 < n_frames; f0 += frames_per_launch) {
+    const int nf = n_frames - f0 < frames_per_launch ? n_frames - f0 : frames_per_launch;
+    const char* rawp = (const char*)raw + (long long)f0 * H * W * eb;
+    char* pl = (char*)planes + (long long)f0 * p.frame_stride * eb;
+    const dim3 grid(gx, (unsigned)(nf * rows_per_frame));
+    if (p.elem_bytes == 1)
+      pack_kernel<uint8_t><<<grid, tpb, 0, st>>>((const uint8_t*)rawp, kind, H, W, p, (uint8_t*)pl);
+    else
+      pack_kernel<uint16_t><<<grid, tpb, 0, st>>>((const uint16_t*)rawp, kind, H, W, p, (uint16_t*)pl);
+    const int rc = cuda_status(cudaGetLastError(), "pack_kernel");
+    if (rc) return rc;
+  }
+  return BMC_OK;
 }
 
 // ---------------------------------------------------------------------------
