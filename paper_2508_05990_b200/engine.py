@@ -133,20 +133,27 @@ class ClipEngine:
             N.ptr(self.acc), N.ptr(self.fsk), N.ptr(self.last_key), N.ptr(self.kind), N.ptr(self.ref),
             N.ptr(self.trigger), self.T, ref_next, self.T, N.stream_handle()))
 
+    def _pack(self) -> None:
+        N.check(N.load().bmc_pack_planes(N.ptr(self.raw), self.S * self.T, self.kind_code, ctypes.byref(self.params),
+                                         N.ptr(self.planes), N.stream_handle()))
+
+    def _estimate_all(self) -> None:
+        arr = self._level_slice(0, self.n_pairs)
+        N.check(N.load().bmc_estimate_motion(N.ptr(self.planes), self.S * self.T, ctypes.byref(self.params),
+                                             self.n_pairs, N.ptr(self.cur_index), N.ptr(self.ref_index), arr,
+                                             N.stream_handle()))
+
     def motion(self) -> None:
         """Pack + ME + refine + AEM decisions for every frame of every stream."""
         lib = N.load()
         p = self.params
         st = N.stream_handle()
-        N.check(lib.bmc_pack_planes(N.ptr(self.raw), self.S * self.T, self.kind_code, ctypes.byref(p),
-                                    N.ptr(self.planes), st))
+        self._pack()
         self._reset_state()
         if self.T < 2:
             return
         if self.cfg.reference_policy == "previous":
-            arr = self._level_slice(0, self.n_pairs)
-            N.check(lib.bmc_estimate_motion(N.ptr(self.planes), self.S * self.T, ctypes.byref(p), self.n_pairs,
-                                            N.ptr(self.cur_index), N.ptr(self.ref_index), arr, st))
+            self._estimate_all()
             self._refine(0, self.n_pairs)
             self._decide(1, self.T)
             return
@@ -159,6 +166,21 @@ class ClipEngine:
             self._refine(lo, hi)
             nxt = N.ptr(self.ref_index[hi:hi + S]) if t + 1 < self.T else None
             self._decide(t, t + 1, nxt)
+
+    def launches_per_step(self) -> int:
+        """Kernels of this library one step launches (pack, ME stages, refine, decide, label chain)."""
+        fme = self.cfg.fme
+        searched = 0
+        for k, st in enumerate(fme.stages):
+            if not (st.range == 0 and k > 0):  # range-0 stages after a searched stage are folded (no launch)
+                searched += 1
+        fpl = max(1, 65535 // (self.params.pad_h * (2 if self.bayer else 1)))  # frames per pack launch
+        pack = -(-(self.S * self.T) // fpl)
+        if self.cfg.reference_policy == "previous" or self.T < 2:
+            motion = searched * len(fme.block_sizes) + (2 if self.T >= 2 else 0)
+        else:
+            motion = (self.T - 1) * (searched * len(fme.block_sizes) + 2)
+        return pack + motion + 1
 
     def _refine(self, lo: int, hi: int) -> None:
         fin = self.levels[-1]
@@ -185,22 +207,54 @@ class ClipEngine:
 
     # ------------------------------------------------------------------ graphs
     def capture(self) -> None:
-        """Capture one full step (motion + predict) as a CUDA graph."""
+        """Capture one full step as CUDA graphs.  With the "previous" policy the
+        step is three graphs -- pack, motion estimation, and refine + AEM +
+        label chain -- so a caller can bracket the ME graph with events
+        (``replay(me_events=...)``) and time the dominant kernel inside a
+        timed step; otherwise one graph."""
         torch = self.torch
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             self.step()  # warm-up: sets kernel attributes, builds tables
         torch.cuda.current_stream().wait_stream(side)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.step()
-        self.graph = g
+        if self.cfg.reference_policy == "previous" and self.T >= 2:
+            graphs = []
+            for part in (self._graph_pre, self._estimate_all, self._graph_post):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    part()
+                graphs.append(g)
+            self.graph = graphs
+        else:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step()
+            self.graph = [g]
 
-    def replay(self) -> None:
+    def _graph_pre(self) -> None:
+        self._pack()
+        self._reset_state()
+
+    def _graph_post(self) -> None:
+        self._refine(0, self.n_pairs)
+        self._decide(1, self.T)
+        self.predict()
+
+    def replay(self, me_events=None) -> None:
+        """Replay the captured step; ``me_events=(start, end)`` are recorded
+        around the motion-estimation graph on the current stream."""
         if self.graph is None:
             self.capture()
-        self.graph.replay()
+        if len(self.graph) == 3 and me_events is not None:
+            self.graph[0].replay()
+            me_events[0].record()
+            self.graph[1].replay()
+            me_events[1].record()
+            self.graph[2].replay()
+            return
+        for g in self.graph:
+            g.replay()
 
     # ------------------------------------------------------------------ results
     def decisions_host(self):
