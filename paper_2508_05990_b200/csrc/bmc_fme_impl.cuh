@@ -441,13 +441,11 @@ __device__ int count_lo(const SmemLayout& L, const StagePlan& pl, const StageGeo
   const int lane = threadIdx.x & 31;
   const int n = pc.P * b * b;
   if (D > pc.max_value) return 0;
-  const int lb = __ffs(b) - 1;
-  const int lwpr = lb - (EPW == 4 ? 2 : 1);  // log2(words per block row)
-  const int words = n / EPW;
+  const int wpr = b / EPW;                     // words per block row (2..16)
+  const int rows_per_iter = 32 / wpr;          // block rows covered by one warp step
+  const int wc = lane % wpr, r0 = lane / wpr;  // fixed word column of this lane
   const bool staged = pl.pg == pc.P;
   const int dx = g.cx + (i - g.r) * g.s, dy = g.cy + (j - g.r) * g.s;
-  uint32_t a1 = 0, a2 = 0;
-  int cnt = 0;
   uint32_t k1, k2;
   if constexpr (EPW == 4) {
     k1 = 0x01010101u * (uint32_t)(D - 1);
@@ -456,20 +454,9 @@ __device__ int count_lo(const SmemLayout& L, const StagePlan& pl, const StageGeo
     k1 = D <= 32768 ? 0x00010001u * (uint32_t)(0x8000 - D) : 0x00010001u * (uint32_t)(0x10000 - D);
     k2 = 0;
   }
-  for (int t = lane; t < words; t += 32) {
-    const int wc = t & ((1 << lwpr) - 1), y = (t >> lwpr) & (b - 1), p = t >> (lwpr + lb);
-    uint32_t cw, rw;
-    if (staged) {
-      cw = ldw_shifted<Elem>(L.cur, (p * b + y) * pl.cbw + coff + wc * EPW);
-      rw = ldw_shifted<Elem>(L.win, (p * pl.wrows + j * g.s + y) * pl.bw + g.d + i * g.s + wc * EPW);
-    } else {
-      const uint32_t* crow = reinterpret_cast<const uint32_t*>(pc.cur + p * pc.plane_stride +
-                                                               (long long)(oy + y) * pc.pitch);
-      const uint32_t* rrow = reinterpret_cast<const uint32_t*>(pc.ref + p * pc.plane_stride +
-                                                               (long long)(oy + dy + y) * pc.pitch);
-      cw = ldw_shifted<Elem>(crow, ox + wc * EPW);
-      rw = ldw_shifted<Elem>(rrow, ox + dx + wc * EPW);
-    }
+  uint32_t a1 = 0, a2 = 0;
+  int cnt = 0;
+  auto count_word = [&](uint32_t cw, uint32_t rw) {
     if constexpr (EPW == 4) {
       const uint32_t d4 = __vabsdiffu4(cw, rw);
       asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(d4), "r"(k1));
@@ -481,6 +468,35 @@ __device__ int count_lo(const SmemLayout& L, const StagePlan& pl, const StageGeo
       const uint32_t d2 = mx - mn;
       const uint32_t f = D <= 32768 ? (((d2 & 0x7fff7fffu) + k1) | d2) : (((d2 & 0x7fff7fffu) + k1) & d2);
       cnt += __popc(f & 0x80008000u);
+    }
+  };
+  if (staged) {
+    // the candidate's window starts at element (g.d + i*s) of each staged row: one shift for all its words
+    const int xoff = g.d + i * g.s;
+    const int sh = (xoff % EPW) * 8 * (int)sizeof(Elem);
+    const int cbw = pl.cbw / EPW, bww = pl.bw / EPW;
+    for (int p = 0; p < pc.P; ++p) {
+      const uint32_t* crow = L.cur + (p * b + r0) * cbw + coff / EPW + wc;
+      const uint32_t* rrow = L.win + (p * pl.wrows + j * g.s + r0) * bww + xoff / EPW + wc;
+      for (int y = r0; y < b; y += rows_per_iter) {
+        const uint32_t lo = rrow[0];
+        count_word(crow[0], sh ? __funnelshift_r(lo, rrow[1], sh) : lo);
+        crow += rows_per_iter * cbw;
+        rrow += rows_per_iter * bww;
+      }
+    }
+  } else {
+    const int xr = ox + dx;  // >= 0 for a valid candidate
+    const int sh = (xr % EPW) * 8 * (int)sizeof(Elem);
+    for (int p = 0; p < pc.P; ++p) {
+      for (int y = r0; y < b; y += rows_per_iter) {
+        const uint32_t* crow = reinterpret_cast<const uint32_t*>(pc.cur + p * pc.plane_stride +
+                                                                 (long long)(oy + y) * pc.pitch) + ox / EPW + wc;
+        const uint32_t* rrow = reinterpret_cast<const uint32_t*>(pc.ref + p * pc.plane_stride +
+                                                                 (long long)(oy + dy + y) * pc.pitch) + xr / EPW + wc;
+        const uint32_t lo = rrow[0];
+        count_word(crow[0], sh ? __funnelshift_r(lo, rrow[1], sh) : lo);
+      }
     }
   }
   if constexpr (EPW == 4) cnt = (int)a1 - (int)a2;
