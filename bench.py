@@ -46,7 +46,15 @@ CONFIGS = {
            "3840x2160 RGGB uint16 60-frame clip, 8x8 blocks, 3-stage +-32 reach, refine + compensate"),
     "c5": (1920, 1080, 40, (24, -16), 7, ((4, 8), (2, 4), (2, 1)), (64, 32), "uint8",
            "1080p RGGB uint8 40-frame high-motion pan, standard preset (64->32 split)"),
+    # C4: 64 independent C2 streams, sharded 64/N per GPU (stream k: seed 1000+k, SURVEY §8d velocities)
+    "c4": (1920, 1080, 30, None, 1000, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
+           "64 streams of 1920x1080 RGGB uint8 30-frame clips, 16x16 blocks, +-16 full search, sharded across GPUs"),
 }
+C4_STREAMS = 64
+
+
+def c4_velocity(k):
+    return (2 * ((k % 9) - 4), 2 * ((k // 9 % 7) - 3))
 
 
 def log(*a):
@@ -64,6 +72,8 @@ def pipeline_config(name):
 def make_clip(name, seed_offset=0):
     from paper_2508_05990_b200 import synth
     w, h, t, v, seed = CONFIGS[name][:5]
+    if v is None:  # c4: per-stream velocity
+        v = c4_velocity(seed_offset)
     dt = np.uint16 if CONFIGS[name][7] == "uint16" else np.uint8
     clip = synth.bayer_pan_clip(w, h, t, v, seed=seed + seed_offset, dtype=dt)
     labels = synth.block_labels(w, h, t, seed=seed + seed_offset)
@@ -216,13 +226,23 @@ def run_b200(args, rank, world, local_rank):
     c = CONFIGS[name]
     W, H, T = c[0], c[1], c[2]
     pcfg = pipeline_config(name)
-    clip, labels = make_clip(name, seed_offset=rank)
+    if name == "c4":
+        if C4_STREAMS % world:
+            raise SystemExit(f"c4 shards {C4_STREAMS} streams: world size {world} must divide it")
+        S = C4_STREAMS // world
+        stream_ids = [rank * S + k for k in range(S)]  # contiguous shard per rank, no hot-path collective
+    else:
+        S = max(1, args.streams)
+        stream_ids = [rank * S + k for k in range(S)]
+    clips = [make_clip(name, seed_offset=sid) for sid in stream_ids]
+    clip, labels = clips[0]
     dt = clip.dtype
 
-    eng = ClipEngine(pcfg, H, W, T, 1, dt, True)
-    eng.load_frames(clip)
-    for t in range(T):
-        eng.key_labels[0, t].copy_(torch.from_numpy(labels[t].classes.copy()))
+    eng = ClipEngine(pcfg, H, W, T, S, dt, True)
+    eng.load_frames(np.stack([c for c, _ in clips]))
+    for k, (_c, labs) in enumerate(clips):
+        for t in range(T):
+            eng.key_labels[k, t].copy_(torch.from_numpy(labs[t].classes.copy()))
     eng.capture()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 512 MB > 126 MB L2
 
@@ -262,38 +282,42 @@ def run_b200(args, rank, world, local_rank):
     samples = sum(e * P * b * b for e, b in zip(evals, pcfg.fme.block_sizes))
     bpp = np.dtype(dt).itemsize
     me_bytes = eng.n_pairs * 2 * bpp * W * H  # cur + ref reads per pair
-    step_bytes = (T - 1) * (2 * bpp * W * H + 2 * W * H)  # frames + label read/write
+    step_bytes = S * (T - 1) * (2 * bpp * W * H + 2 * W * H)  # frames + label read/write
 
     # --- e2e through the public host-buffer API ---
     sess = ClipSession(pcfg, H, W, T, dt, True)
-    raw_pinned = torch.from_numpy(clip).pin_memory()
-    # key labels as one pinned (T, H, W) tensor: only key frames' maps are used, the upload overlaps ME
-    key = torch.from_numpy(np.stack([labels[t].classes for t in range(T)])).pin_memory()
+    # per stream: pinned raw clip + key labels as one pinned (T, H, W) tensor (only key frames' maps are
+    # used; the upload overlaps ME)
+    host_in = [(torch.from_numpy(c).pin_memory(),
+                torch.from_numpy(np.stack([labs[t].classes for t in range(T)])).pin_memory()) for c, labs in clips]
     for _ in range(2):
-        sess.run(raw_pinned, key)
+        for raw_k, key_k in host_in:
+            sess.run(raw_k, key_k)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     e2e_ms = []
+    e2e_ok = True
     for _ in range(args.steps):
         flush_l2()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out_labels, kinds, _refs, _trig = sess.run(raw_pinned, key)
+        for k, (raw_k, key_k) in enumerate(host_in):  # every stream of this rank through the public API
+            out_labels, kinds, _refs, _trig = sess.run(raw_k, key_k)
+            if k == S - 1:
+                e2e_ok = e2e_ok and bool(np.array_equal(out_labels, eng.labels[k].cpu().numpy()))
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    # parity spot check of the e2e result against the graph result
-    e2e_ok = bool(np.array_equal(out_labels, eng.labels[0].cpu().numpy()))
 
     # --- max over ranks (the only collective: one tiny exchange after timing) ---
     from paper_2508_05990_b200 import sharding
-    digest = sharding.parity_hash(eng.labels[0].cpu().numpy(), eng.kind.cpu().numpy())
-    stats = sharding.gather_stats((T - 1) * args.steps, total_ms / 1e3, digest, device=dev)
+    digest = sharding.parity_hash(eng.labels.cpu().numpy(), eng.kind.cpu().numpy())
+    stats = sharding.gather_stats((T - 1) * S * args.steps, total_ms / 1e3, digest, device=dev)
     vals = torch.tensor([total_ms, statistics.mean(e2e_ms), me_avg], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     total_ms, e2e_avg, me_avg = (float(v) for v in vals.tolist())
     ms_per_step = total_ms / args.steps
-    frames = (T - 1) * world
+    frames = (T - 1) * S * world
     value = frames / (ms_per_step / 1e3)
     e2e_value = frames / (e2e_avg / 1e3)
 
@@ -321,7 +345,7 @@ def run_b200(args, rank, world, local_rank):
         "metric": "frames_per_sec", "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8" if bpp == 1 else "u16", "data": "synthetic",
-        "config": {"workload": c[8], "frames_per_step_per_gpu": T - 1, "streams_per_gpu": 1,
+        "config": {"workload": c[8], "frames_per_step_per_gpu": (T - 1) * S, "streams_per_gpu": S,
                    "l2": "flushed (512 MB write) between timed steps", "graph": "3 CUDA graphs per step (pack | ME | refine+AEM+label chain), events around the ME graph",
                    "parallelism": f"stream-sharded x{world} (no hot-path collective)"},
         "roofline": {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Gsamples/s",
@@ -335,8 +359,8 @@ def run_b200(args, rank, world, local_rank):
                              "peak_gbs": hbm_peak}},
         "kernel_share_of_step": me_avg / (total_ms / args.steps),
         "step_bytes_algorithmic": step_bytes,
-        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": sess.h2d_bytes,
-                "d2h_bytes_per_step": sess.d2h_bytes, "ms_per_step": e2e_avg, "labels_match_device_run": e2e_ok},
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": sess.h2d_bytes * S,
+                "d2h_bytes_per_step": sess.d2h_bytes * S, "ms_per_step": e2e_avg, "labels_match_device_run": e2e_ok},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "keyframes_per_clip": int((eng.kind[0] == 0).sum().item()),
@@ -365,6 +389,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=1, help="independent clips per GPU (c4: 64 / world)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))
