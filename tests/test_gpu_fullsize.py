@@ -1,0 +1,134 @@
+"""GPU parity at BASELINE.json's full sizes (1080p, C2 search) through properties and
+sampled oracle checks -- the numpy oracle needs ~12 s per full 1080p pair, so the
+whole-frame comparisons use size-independent properties and the oracle runs on
+sampled blocks and on the cheap downstream stages (refine / decide / predict),
+fed with the GPU's own motion fields.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import bayermc_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W, H = 1920, 1080
+C2_STAGES = ((16, 1), (0, 1), (0, 1))
+
+
+def _c2_cfg():
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    return FmeConfig(stages=tuple(SearchStage(*s) for s in C2_STAGES), block_sizes=(16,))
+
+
+def _ocfg(c):
+    return O.cfg_dict(stages=[(s.range, s.step) for s in c.stages], lam=c.lam, block_sizes=c.block_sizes,
+                      split_threshold=c.split_threshold, sparsity_tolerance=c.sparsity_tolerance,
+                      refine_block_threshold=c.refine_block_threshold)
+
+
+@pytest.fixture(scope="module")
+def c2_clip():
+    from paper_2508_05990_b200 import synth
+    # the bench's C2 recipe (seed 5, v=(4,-2)) plus a textured square moving at an odd velocity so
+    # that the field has real outliers, refinement replacements and sparsity-dominated blocks
+    return synth.bayer_pan_clip(W, H, 6, (4, -2), seed=5, square=160, square_velocity=(7, -3))
+
+
+def _valid_area(pad_h, pad_w, b, r):
+    """Closed-form candidate_evals of a full-search level: sum of valid-rectangle areas."""
+    total = 0
+    for oy in range(0, pad_h, b):
+        ny = min(oy + r, pad_h - b) - max(oy - r, 0) + 1
+        for ox in range(0, pad_w, b):
+            nx = min(ox + r, pad_w - b) - max(ox - r, 0) + 1
+            total += nx * ny
+    return total
+
+
+def test_c2_fullsize_sampled_blocks_match_oracle(cuda, c2_clip):
+    from paper_2508_05990_b200 import fme, synth
+    fr = synth.frames_of(c2_clip)
+    cfg = _c2_cfg()
+    got = fme.estimate_motion(fr[1], fr[0], cfg)[0]
+    pc = O.pad_edge(O.search_planes(c2_clip[1], True), 16)
+    pr = O.pad_edge(O.search_planes(c2_clip[0], True), 16)
+    gh, gw = got.mv.shape[:2]
+    assert (gh, gw) == (34, 60)
+    rng = np.random.default_rng(0)
+    blocks = {(0, 0), (0, gw - 1), (gh - 1, 0), (gh - 1, gw - 1), (gh - 1, gw // 2), (gh // 2, 0)}
+    # the moving square (full-res origin (480, 270)): its blocks and their neighbours
+    for gy in range(7, 16):
+        blocks.add((gy, 15 + (gy % 3)))
+    blocks |= {(int(rng.integers(gh)), int(rng.integers(gw))) for _ in range(24)}
+    o = _ocfg(cfg)
+    for gy, gx in sorted(blocks):
+        mv, e, _n = O.search_block(pc, pr, (gx * 16, gy * 16), 16, (0, 0), o["stages"], o["lam"],
+                                   o["sparsity_tolerance"])
+        assert tuple(got.mv[gy, gx]) == tuple(mv), (gy, gx)
+        assert np.float64(got.energy[gy, gx]).view(np.int64) == np.float64(e).view(np.int64), (gy, gx)
+    # candidate count of the whole frame, closed form
+    assert got.candidate_evals == _valid_area(544, 960, 16, 16) + 2 * gh * gw
+
+
+def test_c2_fullsize_uint16_equals_uint8_times_257(cuda, c2_clip):
+    from paper_2508_05990_b200 import fme, synth
+    f8 = synth.frames_of(c2_clip[:2])
+    f16 = synth.frames_of(c2_clip[:2].astype(np.uint16) * 257)
+    a = fme.estimate_motion(f8[1], f8[0], _c2_cfg())[0]
+    b = fme.estimate_motion(f16[1], f16[0], _c2_cfg())[0]
+    np.testing.assert_array_equal(a.mv, b.mv)
+    np.testing.assert_array_equal(a.energy.view(np.int64), b.energy.view(np.int64))
+    np.testing.assert_array_equal(a.matched, b.matched)
+    assert a.candidate_evals == b.candidate_evals
+
+
+def test_c2_fullsize_identical_frames(cuda, c2_clip):
+    from paper_2508_05990_b200 import fme, synth
+    f = synth.frames_of(c2_clip[:1])[0]
+    out = fme.estimate_motion(f, f, _c2_cfg())[0]
+    assert (out.mv == 0).all() and (out.energy == 0).all() and out.matched.all()
+    assert out.candidate_evals == _valid_area(544, 960, 16, 16) + 2 * 34 * 60
+
+
+@pytest.mark.parametrize("decisions", ["gop4", "threshold"])
+def test_c2_fullsize_downstream_stages_match_oracle(cuda, c2_clip, decisions):
+    """Whole-clip engine at 1080p: refine, AEM decisions and the label chain are
+    checked against the oracle applied to the GPU's own level-0 fields."""
+    from paper_2508_05990_b200 import synth
+    from paper_2508_05990_b200.config import PipelineConfig
+    from paper_2508_05990_b200.engine import ClipEngine
+    T = c2_clip.shape[0]
+    kw = dict(max_gop=4, aem_threshold=float("inf")) if decisions == "gop4" else dict(aem_threshold=0.6)
+    pcfg = PipelineConfig(fme=_c2_cfg(), refine_enabled=False, **kw)
+    labels = synth.block_labels(W, H, T, seed=2)
+    eng = ClipEngine(pcfg, H, W, T)
+    eng.load_frames(c2_clip)
+    for t in range(T):
+        eng.key_labels[0, t].copy_(cuda.from_numpy(labels[t].classes))
+    eng.capture()
+    eng.replay()
+    cuda.cuda.synchronize()
+    mv0, e0, m0, _ = eng.level_host(0)
+    mvr, er, _ = eng.refined_host()
+    kinds, refs, trig = (a[0] for a in eng.decisions_host())
+    got_labels = eng.labels[0].cpu().numpy()
+    o = _ocfg(pcfg.fme)
+    acc = np.zeros((34, 60))
+    fsk = 0
+    out = [labels[0].classes]
+    assert kinds[0] == 0
+    for t in range(1, T):
+        p = eng.pair_index(0, t)
+        field = O.OracleField(16, mv0[p].astype(np.int64), e0[p], m0[p].astype(bool), 0, 0)
+        ref_f = O.refine_mvs(field, 4, O.search_planes(c2_clip[t], True), O.search_planes(c2_clip[t - 1], True), o)
+        np.testing.assert_array_equal(mvr[p], ref_f.mv)
+        np.testing.assert_array_equal(er[p].view(np.int64), ref_f.energy.view(np.int64))
+        kind, ref, tr, acc, fsk = O.decide(acc, fsk, 16, ref_f.energy, 16, t, aem_threshold=pcfg.aem_threshold,
+                                           max_gop=pcfg.max_gop)
+        assert ("key", "nonkey_prev_ref", "nonkey_key_ref")[kinds[t]] == kind
+        assert trig[t] == tr
+        out.append(labels[t].classes if kind == "key" else O.predict_labels(out[ref], ref_f, 2))
+        np.testing.assert_array_equal(got_labels[t], out[t])
+    if decisions == "gop4":
+        assert list(kinds) == [0, 1, 1, 1, 0, 1]
