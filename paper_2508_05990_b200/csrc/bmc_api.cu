@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "bmc_internal.cuh"
@@ -159,6 +160,15 @@ int bmc_pack_planes(const void* raw, int n_frames, int kind, const bmc_fme_param
   return launch_pack(raw, n_frames, kind, *p, planes, (cudaStream_t)stream);
 }
 
+static int stage_kblk() {
+  static const int v = [] {
+    const char* e = getenv("BMC_KBLK");
+    const int k = e ? atoi(e) : 2;
+    return k >= 1 && k <= 8 ? k : 2;
+  }();
+  return v;
+}
+
 int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* p, int n_pairs,
                         const int32_t* cur_index, const int32_t* ref_index, bmc_level_out* levels, void* stream) {
   int rc = check_params(p);
@@ -192,7 +202,14 @@ int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* 
       const int s = launched[k];
       StageLaunch a;
       std::memset(&a, 0, sizeof a);
-      rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true);
+      // level 0's first searched stage is centred on (0, 0) for every block: kblk horizontally
+      // adjacent blocks share one staged window (fme.py:350-368 with mv = 0 at level 0)
+      a.kblk = (L == 0 && k == 0) ? stage_kblk() : 1;
+      rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, a.kblk);
+      if (rc == BMC_OK && a.kblk > 1 && !a.plan.use_tma) {
+        a.kblk = 1;
+        rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, 1);
+      }
       if (rc) return rc;
       a.planes = planes;
       a.ref_planes = planes;
@@ -220,7 +237,7 @@ int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* 
       a.matched = levels[L].matched;
       a.evals = levels[L].evals;
       a.tab16 = tab16;
-      rc = launch_fme_stage(a, n_frames, n_frames, dim3(a.gw * a.gh, n_pairs), st);
+      rc = launch_fme_stage(a, n_frames, n_frames, dim3((a.gw + a.kblk - 1) / a.kblk * a.gh, n_pairs), st);
       if (rc) return rc;
     }
   }
@@ -247,7 +264,8 @@ int bmc_search_stage(const void* cur_planes, const void* ref_planes, const bmc_f
   StageLaunch a;
   std::memset(&a, 0, sizeof a);
   // arbitrary origins: plain-load staging (TMA tiles need 16-byte aligned starts)
-  rc = plan_stage(a.plan, *p, block_size, search_range, step, false);
+  a.kblk = 1;
+  rc = plan_stage(a.plan, *p, block_size, search_range, step, false, 1);
   if (rc) return rc;
   a.planes = cur_planes;
   a.ref_planes = ref_planes;

@@ -68,7 +68,7 @@ static const int kSmemTarget = 110 * 1024;
 // CTA) unless shared memory already limits the SM to <= 2 CTAs, where bigger
 // CTAs are the only source of parallelism.  `smem_fixed` is the CTA's shared
 // memory without the per-part partial-sum arrays.
-static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed) {
+static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed, int kblk) {
   static const int max_threads = [] {
     const char* e = getenv("BMC_MAX_THREADS");
     const int v = e ? atoi(e) : kMaxStageThreads;
@@ -77,10 +77,10 @@ static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed) {
   int best_parts = 1, best_threads = 64;
   double best_u = -1.0;
   for (int parts = 1; parts <= units_max; ++parts) {
-    const int smem = smem_fixed + ((parts * pl.nmax * 4 + 127) & ~127);
+    const int smem = smem_fixed + ((kblk * parts * pl.nmax * 4 + 127) & ~127);
     const int by_smem = (228 * 1024) / (smem + 1024);
     const int cap = by_smem <= 2 ? max_threads : (max_threads < 256 ? max_threads : 256);
-    const int items = cols * parts;
+    const int items = cols * parts * kblk;
     int threads = (items + 31) / 32 * 32;
     if (threads > cap) threads = cap;
     if (threads < 64) threads = 64;
@@ -101,13 +101,13 @@ static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed) {
   pl.threads = best_threads;
 }
 
-int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma) {
+int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma, int kblk) {
   std::memset(&pl, 0, sizeof pl);
   const int eb = p.elem_bytes, epw = 4 / eb;
   const int G = 2 * r + 1;
   pl.ty = pick_ty(G);
   pl.nmax = G * G;
-  const int wwin = 2 * r * s + b;
+  const int wwin = 2 * r * s + b * kblk;  // kblk adjacent blocks share the window
   const int align = 16 / eb;  // TMA: inner box extent and start coordinate on 16-byte boundaries
   static const bool no_tma = [] {
     const char* e = getenv("BMC_NO_TMA");
@@ -121,14 +121,14 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
   const int bw_tma = (wwin + (align - 1) + epw + align - 1) / align * align;
   pl.use_tma = (allow_tma && !no_tma && bw_tma <= 256 && wwin <= 256) ? 1 : 0;
   pl.bw = pl.use_tma ? bw_tma : (wwin + epw + align - 1) / align * align;
-  pl.hwin = wwin;
   const int cw_words = (b / epw) >= 4 ? 4 : 2;
   const int chunks = (b / epw) / cw_words;
   // plane stride in smem = hwin rows (the 3-D TMA box is written densely); the
   // padding rows of the last row group run into the next plane (harmless: their
   // sums are discarded) and past the last plane into ty*s slack rows.
-  pl.wrows = wwin;
-  pl.cbw = pl.use_tma ? (b * eb >= 16 ? b : align) : b;
+  pl.hwin = 2 * r * s + b;  // rows: blocks are adjacent horizontally only
+  pl.wrows = pl.hwin;
+  pl.cbw = pl.use_tma ? (b * kblk * eb >= 16 ? b * kblk : align) : b * kblk;
   // sub-word candidate offsets: with TMA the window starts up to align-1
   // elements into the box, so any phase can occur; plain-load staging stores
   // the window unshifted, so only step % epw != 0 produces sub-word phases.
@@ -142,10 +142,10 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
       {
         const int fixed = ((head + 127) & ~127) + ((2 * q.nmax * 4 + 127) & ~127) +
                           ((pg * b * q.cbw * eb + 127) & ~127) + (pg * q.wrows + q.ty * s) * q.bw * eb;
-        pick_parts(q, cols, pg * chunks * (s < b ? s : b), fixed);
+        pick_parts(q, cols, pg * chunks * (s < b ? s : b), fixed, kblk);
       }
       const int off_sad = (head + 127) & ~127;
-      const int off_klist = off_sad + ((q.parts * q.nmax * 4 + 127) & ~127);
+      const int off_klist = off_sad + ((kblk * q.parts * q.nmax * 4 + 127) & ~127);
       const int off_cur = off_klist + ((2 * q.nmax * 4 + 127) & ~127);  // klist + klist2
       const int cur_bytes = pg * b * q.cbw * eb;
       const int win_bytes = (pg * q.wrows + q.ty * s) * q.bw * eb;

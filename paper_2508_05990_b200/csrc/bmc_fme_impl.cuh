@@ -335,7 +335,7 @@ __device__ __forceinline__ void sad_run(const uint32_t* rp, const uint32_t* cp, 
 // pass (the item -> thread mapping is identical in every pass).
 template <typename Elem, int CW, int TY, bool SHIFT>
 __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int npl, const StagePlan& pl, int coff_w,
-                          bool add) {
+                          bool add, int nblk) {
   constexpr int EPW = 4 / sizeof(Elem);
   const int nt = blockDim.x;
   const int bww = pl.bw / EPW;
@@ -347,15 +347,16 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   const int parts = pl.parts;
   const int per = (units + parts - 1) / parts;
   const int cols = g.G * g.ncg;
-  const int items = cols * parts;
+  const int items = cols * parts * nblk;  // nblk horizontally adjacent blocks share the staged window
   const int rstep = s * bww, cstep = s * cbw;
   const int N = g.G * g.G;
-  const FastDiv fG(g.G), fncg(g.ncg), frho(nrho), fcpr(cpr), fs(s);
+  const FastDiv fG(g.G), fncg(g.ncg), frho(nrho), fcpr(cpr), fs(s), fparts(parts);
   for (int it = threadIdx.x; it < items; it += nt) {
-    uint32_t q, i, gi, part;
+    uint32_t q, i, gi, part, kb;
     fG.divmod(it, q, i);
     fncg.divmod(q, part, gi);
-    const int xo = g.d + i * s;
+    fparts.divmod(part, kb, part);
+    const int xo = g.d + kb * b + i * s;
     const int ph = xo % EPW;
     const uint32_t* win = (SHIFT || ph == 0) ? L.win : L.win + (pl.copies == 2 ? 1 : ph) * pl.copy_words;
     const int sh = ph * 8 * (int)sizeof(Elem);
@@ -370,11 +371,11 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
       // window rows past hwin (next plane / slack rows) only feed the padding
       // candidates of the last row group, whose sums are discarded.
       const uint32_t* R0 = win + pp * pl.wrows * bww + (xo / EPW) + c * CW;
-      const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + c * CW;
+      const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + kb * (b / EPW) + c * CW;
       const int M = (int)fs.div(b - 1 - rho) + 1;
       sad_run<Elem, CW, TY, SHIFT>(R0 + (rho + gi * TY * s) * bww, C0 + rho * cbw, rstep, cstep, M, sh, acc);
     }
-    uint32_t* dst = L.sad + part * N;
+    uint32_t* dst = L.sad + (kb * parts + part) * N;
 #pragma unroll
     for (int j = 0; j < TY; ++j) {
       const int jj = gi * TY + j;
@@ -504,11 +505,13 @@ __device__ int count_lo(const SmemLayout& L, const StagePlan& pl, const StageGeo
   return EPW == 4 ? (cnt + n) / 2 : cnt;
 }
 
-// One stage for one block; all threads participate and receive the result.
+// Staging + integer SAD of one stage for nblk horizontally adjacent blocks
+// sharing one search centre (nblk > 1 only for level 0's first searched stage,
+// whose centre is (0, 0) for every block).  All threads participate.
 template <typename Elem, int CW, int TY, bool SHIFT>
-__device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
-                                    const CUtensorMap* tm_win, const CUtensorMap* tm_cur, uint32_t& phase, int ox,
-                                    int oy, int b, int cx, int cy, int r, int s) {
+__device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
+                               const CUtensorMap* tm_win, const CUtensorMap* tm_cur, uint32_t& phase, int ox, int oy,
+                               int b, int cx, int cy, int r, int s, int nblk, int& coff_e) {
   constexpr int EPW = 4 / sizeof(Elem);
   StageGeom g;
   g.r = r;
@@ -525,11 +528,8 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   g.d = g.wx0 - g.tx0;
   const int cx0 = pl.use_tma ? ox - (ox % A16) : ox;  // ox >= 0
   const int coff_w = (ox - cx0) / EPW;
-  const int coff_e = ox - cx0;  // element offset of the block inside each staged cur row
-  const int N = g.G * g.G;
-  const int nt = blockDim.x, nw = nt >> 5;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = pc.P * b * b;
+  coff_e = ox - cx0;  // element offset of the block inside each staged cur row
+  const int tid = threadIdx.x;
   // sub-word phases used by this CTA's candidate columns
   unsigned phase_mask = 0;
   if (!SHIFT && pl.copies)
@@ -556,10 +556,23 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
       build_phase_copies<Elem>(L, pl, npl, phase_mask);
     }
     __syncthreads();
-    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0);
+    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0, nblk);
   }
   __syncthreads();
+  return g;
+}
 
+// Exact selection for one block of the staged set (block kb: its window starts
+// kb*b elements further into the staged rows, its partial sums at sad).
+// All threads participate and receive the result.
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
+                                    const StageGeom& g, uint32_t* sad, int ox, int oy, int b, int coff_e) {
+  const int r = g.r, s = g.s, cx = g.cx, cy = g.cy;
+  const int N = g.G * g.G;
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = pc.P * b * b;
   // valid candidates form a rectangle i in [ilo, ihi] x j in [jlo, jhi] (fme.py:250-253)
   const int ilo = max(0, r - floor_div(ox + cx, s)), ihi = min(g.G - 1, r + floor_div(pc.frame_w - b - ox - cx, s));
   const int jlo = max(0, r - floor_div(oy + cy, s)), jhi = min(g.G - 1, r + floor_div(pc.frame_h - b - oy - cy, s));
@@ -580,9 +593,9 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
     for (int v = tid; v < res.nvalid; v += nt) {
       const int jv = fwi.div(v);
       const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
-      uint32_t sk = L.sad[k];
-      for (int q = 1; q < parts; ++q) sk += L.sad[q * N + k];
-      if (parts > 1) L.sad[k] = sk;  // the contender passes read the folded sums
+      uint32_t sk = sad[k];
+      for (int q = 1; q < parts; ++q) sk += sad[q * N + k];
+      if (parts > 1) sad[k] = sk;  // the contender passes read the folded sums
       const unsigned long long key = ((unsigned long long)sk << 32) | (unsigned)k;
       best = key < best ? key : best;
     }
@@ -644,7 +657,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   for (int v = tid; v < res.nvalid; v += nt) {
     const int jv = fwi.div(v);
     const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
-    if (k != m0 && L.sad[k] <= sthr) L.klist[atomicAdd(&L.misc[3], 1)] = k;
+    if (k != m0 && sad[k] <= sthr) L.klist[atomicAdd(&L.misc[3], 1)] = k;
   }
   __syncthreads();
   int nk = L.misc[3];
@@ -659,7 +672,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
     for (int e = warp; e < nk; e += nw) {
       const int k = L.klist[e];
       const int clo = count_lo<Elem>(L, pl, g, pc, ox, oy, b, coff_e, k % g.G, k / g.G, D);
-      const double elb = __dadd_rn(__dmul_rn(pc.oml, __ddiv_rn((double)L.sad[k], unit)),
+      const double elb = __dadd_rn(__dmul_rn(pc.oml, __ddiv_rn((double)sad[k], unit)),
                                    __dmul_rn(pc.lam, __ddiv_rn((double)clo, (double)n)));
       if (lane == 0 && elb - kScreenEps <= lim) L.klist2[atomicAdd(&L.misc[5], 1)] = k;
     }
@@ -703,6 +716,18 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   return res;
 }
 
+
+// One stage for one block (the single-block path).
+template <typename Elem, int CW, int TY, bool SHIFT>
+__device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
+                                    const CUtensorMap* tm_win, const CUtensorMap* tm_cur, uint32_t& phase, int ox,
+                                    int oy, int b, int cx, int cy, int r, int s) {
+  int coff_e;
+  const StageGeom g = stage_sad<Elem, CW, TY, SHIFT>(L, pc, pl, tm_win, tm_cur, phase, ox, oy, b, cx, cy, r, s, 1,
+                                                     coff_e);
+  return select_block<Elem, CW, TY, SHIFT>(L, pc, pl, g, L.sad, ox, oy, b, coff_e);
+}
+
 // ---------------------------------------------------------------------------
 // the stage kernel
 // ---------------------------------------------------------------------------
@@ -720,7 +745,8 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
   // over the (pair, block) work list, so the prologue and the per-stage
   // constants are paid once per CTA, not once per block.
   const uint32_t cells = (uint32_t)a.gw * a.gh;
-  const uint32_t total = a.single ? 1u : cells * (uint32_t)a.n_pairs;
+  const uint32_t total = a.single ? 1u
+                                  : (uint32_t)((a.gw + a.kblk - 1) / a.kblk) * a.gh * (uint32_t)a.n_pairs;
   for (uint32_t work = blockIdx.x; work < total; work += gridDim.x) {
     int pair = 0, gx = 0, gy = 0, ox, oy, sx = 0, sy = 0;
     long long cell = 0;
@@ -729,6 +755,61 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
       oy = a.oy;
       sx = a.cx;
       sy = a.cy;
+    } else if (a.kblk > 1) {
+      // nblk horizontally adjacent blocks of level 0's first stage share one window (centre (0, 0))
+      const uint32_t gwg = (a.gw + a.kblk - 1) / a.kblk;
+      const uint32_t cg = gwg * a.gh;
+      pair = (int)(work / cg);
+      const int blk = (int)(work - (uint32_t)pair * cg);
+      const int gx0 = (blk % gwg) * a.kblk;
+      gy = blk / gwg;
+      const int nb = min(a.kblk, a.gw - gx0);
+      PairCtx<Elem> pc;
+      const int cur_f = a.cur_index[pair], ref_f = a.ref_index[pair];
+      pc.cur = reinterpret_cast<const Elem*>(a.planes) + (long long)cur_f * p.frame_stride;
+      pc.ref = reinterpret_cast<const Elem*>(a.ref_planes) + (long long)ref_f * p.frame_stride;
+      pc.cur_z = cur_f * p.planes;
+      pc.ref_z = ref_f * p.planes;
+      pc.pitch = p.pitch;
+      pc.plane_stride = p.plane_stride;
+      pc.frame_h = p.pad_h;
+      pc.frame_w = p.pad_w;
+      pc.P = p.planes;
+      pc.max_value = p.max_value;
+      pc.tol = p.sparsity_tolerance;
+      pc.lam = p.lam;
+      pc.oml = p.one_minus_lam;
+      pc.tab = sizeof(Elem) == 1 ? L.tab : a.tab16;
+      const int ox0 = gx0 * b;
+      oy = gy * b;
+      int coff_e;
+      const StageGeom g = stage_sad<Elem, CW, TY, SHIFT>(L, pc, a.plan, &tm_win, &tm_cur, phase, ox0, oy, b, 0, 0,
+                                                         a.r, a.s, a.kblk, coff_e);
+      const int nsad = a.plan.parts * g.G * g.G;
+      for (int kb = 0; kb < nb; ++kb) {
+        StageGeom gk = g;
+        gk.d += kb * b;
+        const StageResult res = select_block<Elem, CW, TY, SHIFT>(L, pc, a.plan, gk, L.sad + kb * nsad, ox0 + kb * b,
+                                                                  oy, b, coff_e + kb * b);
+        if (threadIdx.x == 0) {
+          const long long c = (long long)pair * cells + (long long)gy * a.gw + gx0 + kb;
+          a.mv[2 * c] = res.dx;
+          a.mv[2 * c + 1] = res.dy;
+          a.energy[c] = res.energy;
+          if (a.last) {
+            bool m;
+            if (a.final_level) {
+              const bool in_real = oy < p.real_h && ox0 + kb * b < p.real_w;  // fme.py:377-384
+              m = !(res.energy > p.refine_block_threshold && in_real);
+            } else {
+              m = res.energy <= p.split_threshold;  // fme.py:386
+            }
+            a.matched[c] = m ? 1 : 0;
+          }
+          atomicAdd(a.evals + pair, (unsigned long long)(res.nvalid + a.extra_evals));
+        }
+      }
+      continue;
     } else {
       pair = (int)(work / cells);
       const int blk = (int)(work - (uint32_t)pair * cells);

@@ -40,6 +40,7 @@ struct StageLaunch {
   const int32_t* cur_index;
   const int32_t* ref_index;
   int level, final_level, b, gw, gh, n_pairs;
+  int kblk;                 // horizontally adjacent blocks per CTA (shared-centre stages), >= 1
   int first, last;          // first / last searched stage of the level
   int r, s;
   int extra_evals;          // range-0 stages folded into this launch's candidate count
@@ -100,7 +101,7 @@ struct PredictArgs {
   int gh, gw, B, scale;
 };
 
-int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma);
+int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma, int kblk = 1);
 int launch_fme_stage(const StageLaunch& a, int n_cur_frames, int n_ref_frames, dim3 grid, cudaStream_t st);
 int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p, void* planes, cudaStream_t st);
 int launch_refine(const RefineArgs& a, cudaStream_t st);
