@@ -17,7 +17,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "lib" / "libbmc_b200.so"
-SOURCES = ["bmc_api.cu", "bmc_fme.cu", "bmc_fme_k_u8c4.cu", "bmc_fme_k_u8c2.cu", "bmc_fme_k_u16.cu", "bmc_ops.cu"]
+SOURCES = ["bmc_api.cu", "bmc_fme.cu", "bmc_fme_k_u8c4.cu", "bmc_fme_k_u8c2.cu", "bmc_fme_k_u16.cu", "bmc_fme_small.cu",
+           "bmc_ops.cu"]
 HEADERS = ["bmc_internal.cuh", "bmc_launch.cuh", "bmc_fme_impl.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]

@@ -198,6 +198,36 @@ int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* 
     const int b = p->block_sizes[L];
     rc = cuda_status(cudaMemsetAsync(levels[L].evals, 0, sizeof(unsigned long long) * n_pairs, st), "memset evals");
     if (rc) return rc;
+    if (small_level_ok(*p, b)) {
+      // small blocks: one warp per block runs the level's three chained stages (bmc_fme_small.cu)
+      StageLaunch a;
+      std::memset(&a, 0, sizeof a);
+      a.planes = planes;
+      a.ref_planes = planes;
+      a.prm = *p;
+      a.cur_index = cur_index;
+      a.ref_index = ref_index;
+      a.level = L;
+      a.final_level = L == p->n_levels - 1;
+      a.b = b;
+      a.gw = p->pad_w / b;
+      a.gh = p->pad_h / b;
+      a.n_pairs = n_pairs;
+      a.kblk = 1;
+      if (L) {
+        a.parent_mv = levels[L - 1].mv;
+        a.parent_e = levels[L - 1].energy;
+        a.parent_matched = levels[L - 1].matched;
+      }
+      a.mv = levels[L].mv;
+      a.energy = levels[L].energy;
+      a.matched = levels[L].matched;
+      a.evals = levels[L].evals;
+      a.tab16 = tab16;
+      rc = launch_fme_small(a, st);
+      if (rc) return rc;
+      continue;
+    }
     for (int k = 0; k < nl; ++k) {
       const int s = launched[k];
       StageLaunch a;

@@ -103,6 +103,8 @@ struct PredictArgs {
 
 int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma, int kblk = 1);
 int launch_fme_stage(const StageLaunch& a, int n_cur_frames, int n_ref_frames, dim3 grid, cudaStream_t st);
+bool small_level_ok(const bmc_fme_params& p, int b);
+int launch_fme_small(const StageLaunch& a, cudaStream_t st);
 int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p, void* planes, cudaStream_t st);
 int launch_refine(const RefineArgs& a, cudaStream_t st);
 int launch_decide(const DecideArgs& a, cudaStream_t st);
