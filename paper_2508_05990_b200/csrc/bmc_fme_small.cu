@@ -33,13 +33,13 @@ constexpr int kSmallWarps = 8;               // blocks per CTA
 constexpr int kSmallCurWords = 256 / 2 + 8;  // 256 uint16 samples (or 256 uint8 + slack) per block
 constexpr double kEps = 1e-11;
 
-template <typename Elem>
-__device__ __forceinline__ void word_sc(uint32_t cw, uint32_t rw, uint32_t& S, int& C, uint32_t k1, uint32_t k2,
-                                        uint32_t& a1, uint32_t& a2, int D) {
+template <typename Elem, bool HIGHD>
+__device__ __forceinline__ void word_sc(uint32_t cw, uint32_t rw, uint32_t& S, uint32_t& C, uint32_t k1, uint32_t k2,
+                                        uint32_t& a2) {
   if constexpr (sizeof(Elem) == 1) {
     const uint32_t d4 = __vabsdiffu4(cw, rw);
     S = __dp4a(d4, 0x01010101u, S);
-    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(d4), "r"(k1));
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(C) : "r"(d4), "r"(k1));
     asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a2) : "r"(d4), "r"(k2));
   } else {
     uint32_t mx, mn;
@@ -47,8 +47,36 @@ __device__ __forceinline__ void word_sc(uint32_t cw, uint32_t rw, uint32_t& S, i
     asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(cw), "r"(rw));
     const uint32_t d2 = mx - mn;
     S = __dp2a_lo(d2, 0x0101u, S);
-    const uint32_t f = D <= 32768 ? (((d2 & 0x7fff7fffu) + k1) | d2) : (((d2 & 0x7fff7fffu) + k1) & d2);
+    const uint32_t f = HIGHD ? (((d2 & 0x7fff7fffu) + k1) & d2) : (((d2 & 0x7fff7fffu) + k1) | d2);
     C += __popc(f & 0x80008000u);
+  }
+}
+
+// (S, C_lo) of one candidate: P planes x b rows of WPR words, reference rows
+// read through L1 with one funnel shift per word (shift 0 for aligned rows).
+template <typename Elem, int WPR, bool HIGHD>
+__device__ __forceinline__ void cand_sc(const uint32_t* __restrict__ rrow, long long rpitch_w, long long rplane_w,
+                                        const uint32_t* crow, int P, int b, int sh, uint32_t k1, uint32_t k2,
+                                        uint32_t& S, uint32_t& C, uint32_t& a2) {
+  for (int pl = 0; pl < P; ++pl) {
+    const uint32_t* rr = rrow + pl * rplane_w;
+    for (int y = 0; y < b; ++y) {
+      uint32_t w[WPR + 1];
+#pragma unroll
+      for (int q = 0; q <= WPR; ++q) w[q] = __ldg(rr + q);
+      uint32_t c[WPR];
+      if constexpr (WPR == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(crow);
+        c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(crow);
+        c[0] = v.x; c[1] = v.y;
+      }
+#pragma unroll
+      for (int q = 0; q < WPR; ++q) word_sc<Elem, HIGHD>(c[q], __funnelshift_r(w[q], w[q + 1], sh), S, C, k1, k2, a2);
+      rr += rpitch_w;
+      crow += WPR;
+    }
   }
 }
 
@@ -89,6 +117,7 @@ __device__ SmallStage small_stage(const Elem* __restrict__ cur_g, const Elem* __
   } else {
     k1 = D <= 32768 ? 0x00010001u * (uint32_t)(0x8000 - D) : 0x00010001u * (uint32_t)(0x10000 - D);
   }
+  const bool highd = EPW == 2 && D > 32768;
   const double unit = (double)p.max_value * (double)n;
   // lane-per-candidate screening: (S, E_lb) of every valid candidate
   uint32_t bestS = 0xffffffffu;
@@ -112,24 +141,17 @@ __device__ SmallStage small_stage(const Elem* __restrict__ cur_g, const Elem* __
     const int dx = cx + (i - r) * s, dy = cy + (j - r) * s;
     const int xr = ox + dx;
     const int sh = (xr % EPW) * 8 * (int)sizeof(Elem);
-    uint32_t S = 0, a1 = 0, a2 = 0;
-    int C = 0;
-    for (int pl = 0; pl < P; ++pl) {
-      const Elem* rplane = ref + (long long)pl * p.plane_stride;
-      for (int y = 0; y < b; ++y) {
-        const uint32_t* rrow = reinterpret_cast<const uint32_t*>(rplane + (long long)(oy + dy + y) * p.pitch) + xr / EPW;
-        const uint32_t* crow = cur_s + (pl * b + y) * wpr;
-        uint32_t lo = __ldg(rrow);
-        for (int w = 0; w < wpr; ++w) {
-          const uint32_t hi = sh ? __ldg(rrow + w + 1) : 0u;
-          const uint32_t rw = sh ? __funnelshift_r(lo, hi, sh) : lo;
-          if (!sh && w + 1 < wpr) lo = __ldg(rrow + w + 1);
-          if (sh) lo = hi;
-          word_sc<Elem>(crow[w], rw, S, C, k1, k2, a1, a2, D);
-        }
-      }
+    uint32_t S = 0, Cacc = 0, a2 = 0;
+    const uint32_t* rrow = reinterpret_cast<const uint32_t*>(ref + (long long)(oy + dy) * p.pitch) + xr / EPW;
+    const long long rpw = p.pitch / EPW, rplw = p.plane_stride / EPW;
+    if (wpr == 4) {
+      if (highd) cand_sc<Elem, 4, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      else cand_sc<Elem, 4, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+    } else {
+      if (highd) cand_sc<Elem, 2, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      else cand_sc<Elem, 2, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
     }
-    if constexpr (EPW == 4) C = ((int)a1 - (int)a2 + n) / 2;
+    int C = EPW == 4 ? ((int)Cacc - (int)a2 + n) / 2 : (int)Cacc;
     if (!count) C = 0;
     const int k = j * G + i;
     const double lb = __dadd_rn(__dmul_rn(p.one_minus_lam, __ddiv_rn((double)S, unit)),
@@ -286,8 +308,10 @@ bool small_level_ok(const bmc_fme_params& p, int b) {
   }();
   if (off) return false;
   if (p.planes * b * b > 256 || b < 8) return false;
+  const int wpr = b * p.elem_bytes / 4;  // words per block row: the kernel is instantiated for 2 and 4
+  if (wpr != 2 && wpr != 4) return false;
   for (int k = 0; k < 3; ++k)
-    if (2 * p.stage_range[k] + 1 > 17) return false;  // per-lane candidate slots (9 rounds of 32)
+    if (2 * p.stage_range[k] + 1 > 17) return false;  // per-lane candidate slots (10 rounds of 32)
   return true;
 }
 

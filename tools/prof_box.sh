@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 for spec in "$@"; do
   cfg=${spec%%:*}; skip=${spec##*:}
   rep=gpurun_out/p_${tag}_${cfg}_s${skip}
-  timeout 600 env $PROF_ENV ncu --set full --clock-control none --import-source on -k regex:fme_ -s $skip -c 1 -o $rep \
+  timeout 600 env $PROF_ENV ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-fme_} -s $skip -c 1 -o $rep \
       python tools/prof_me.py $cfg 1 > $rep.log 2>&1
   python tools/ncu_summary.py $rep.ncu-rep > $rep.txt 2>&1
   python tools/ncu_lines.py $rep.ncu-rep 25 >> $rep.txt 2>&1
