@@ -162,7 +162,7 @@ class ClipSession:
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True, chunks: int = 3):
+                 bayer: bool = True, chunks: int = 6):
         if config.refine_enabled:
             raise NotImplementedError("CaBR-Net block refinement is not part of the B200 hot path yet; "
                                       "run with PipelineConfig(refine_enabled=False)")
@@ -200,6 +200,63 @@ class ClipSession:
             h2d += lab.classes.nbytes
         return h2d
 
+    def _run_streamed(self, src, label_tensor, h2d):
+        """Fully chunked pass ("previous" policy, labels as a tensor): per frame chunk
+        H2D (raw + label maps) -> pack -> ME -> refine -> AEM scan (resumable state)
+        -> label chain -> D2H, so copies in both directions overlap the kernels of
+        neighbouring chunks.  Every step only needs frames of its own or earlier
+        chunks (pair t uses frames t-1, t; the AEM scan and the label chain are
+        causal), so results equal the whole-clip pass."""
+        eng, torch = self.eng, self.torch
+        lib = N.load()
+        cs = torch.cuda.current_stream()
+        st = N.stream_handle(cs)
+        p = eng.params
+        fstride = p.frame_stride
+        esz = eng.planes.element_size()
+        cells2 = eng.gh * eng.gw * 2
+        fs = eng.Hl * eng.Wl
+        eng._reset_state()
+        self.copy_in.wait_stream(cs)  # previous users of the input buffers are done
+        for f0, f1 in self.chunks:
+            ev_in = torch.cuda.Event()
+            with torch.cuda.stream(self.copy_in):
+                eng.raw[0, f0:f1].copy_(src[f0:f1], non_blocking=True)
+                eng.key_labels[0, f0:f1].copy_(label_tensor[f0:f1], non_blocking=True)
+                ev_in.record(self.copy_in)
+            cs.wait_event(ev_in)
+            N.check(lib.bmc_pack_planes(N.ptr(eng.raw[0, f0]), f1 - f0, eng.kind_code, ctypes.byref(p),
+                                        N.ptr(eng.planes) + f0 * fstride * esz, st))
+            p0, p1 = max(f0, 1) - 1, f1 - 1
+            if p1 > p0:
+                arr = eng._level_slice(p0, p1)
+                N.check(lib.bmc_estimate_motion(N.ptr(eng.planes), eng.S * eng.T, ctypes.byref(p), p1 - p0,
+                                                N.ptr(eng.cur_index[p0:p1]), N.ptr(eng.ref_index[p0:p1]), arr, st))
+                eng._refine(p0, p1)
+                eng._decide(p0 + 1, p1 + 1)
+            N.check(lib.bmc_predict_labels_clip(
+                N.ptr(eng.labels), fs, eng.T * fs, N.ptr(eng.key_labels), eng.S, f0, f1, N.ptr(eng.kind),
+                N.ptr(eng.ref), eng.T, eng.Hl, eng.Wl, N.ptr(eng.mv_ref) - 4 * eng.S * cells2,
+                eng.S * cells2, cells2, eng.gh, eng.gw, eng.b_final, eng.scale, N.ptr(eng.workspace), st))
+            ev_out = torch.cuda.Event()
+            ev_out.record(cs)
+            with torch.cuda.stream(self.copy_out):
+                self.copy_out.wait_event(ev_out)
+                self.pin_labels[f0:f1].copy_(eng.labels[0, f0:f1], non_blocking=True)
+        dec = torch.stack([eng.kind[0].double(), eng.ref[0].double(), eng.trigger[0]])
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        with torch.cuda.stream(self.copy_out):
+            self.copy_out.wait_event(ev)
+            self.pin_dec.copy_(dec, non_blocking=True)
+        self.copy_out.synchronize()
+        kinds = self.pin_dec[0].numpy().astype(np.int32)
+        refs = self.pin_dec[1].numpy().astype(np.int32)
+        trig = self.pin_dec[2].numpy().copy()
+        self.h2d_bytes = h2d + label_tensor.numel()
+        self.d2h_bytes = self.pin_dec.numel() * 8 + self.pin_labels.numel()
+        return self.pin_labels.numpy(), kinds, refs, trig
+
     def run(self, raw, key_labels):
         eng, torch = self.eng, self.torch
         lib = N.load()
@@ -221,6 +278,8 @@ class ClipSession:
         esz = eng.planes.element_size()
         eng._reset_state()
         pipelined = eng.cfg.reference_policy == "previous" and eng.T >= 2
+        if pipelined and label_tensor is not None:
+            return self._run_streamed(src, label_tensor, h2d)
         if pipelined:
             for f0, f1 in self.chunks:
                 ev = torch.cuda.Event()
