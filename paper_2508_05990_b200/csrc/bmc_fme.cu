@@ -79,7 +79,12 @@ static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed, i
   for (int parts = 1; parts <= units_max; ++parts) {
     const int smem = smem_fixed + ((kblk * parts * pl.nmax * 4 + 127) & ~127);
     const int by_smem = (228 * 1024) / (smem + 1024);
-    const int cap = by_smem <= 2 ? max_threads : (max_threads < 256 ? max_threads : 256);
+    static const int soft_cap = [] {
+      const char* e = getenv("BMC_CTA_CAP");
+      const int v = e ? atoi(e) : 256;
+      return v >= 64 && v <= kMaxStageThreads ? v / 32 * 32 : 256;
+    }();
+    const int cap = by_smem <= 2 ? max_threads : (max_threads < soft_cap ? max_threads : soft_cap);
     const int items = cols * parts * kblk;
     int threads = (items + 31) / 32 * 32;
     if (threads > cap) threads = cap;
@@ -177,6 +182,11 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     try_plan(alt, false);
     if (alt.pg > pl.pg) pl = alt;
   }
+  static const int debug_skip = [] {
+    const char* e = getenv("BMC_DEBUG_SKIP");
+    return e ? atoi(e) : 0;
+  }();
+  pl.debug = debug_skip;
   if (!pl.pg) {
     set_error("search window of block %d with range %d step %d exceeds the %d KB shared-memory budget", b, r, s,
               kSmemBudget / 1024);

@@ -556,7 +556,11 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
       build_phase_copies<Elem>(L, pl, npl, phase_mask);
     }
     __syncthreads();
-    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0, nblk);
+    if (!(pl.debug & 2)) {
+      sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0, nblk);
+    } else {  // measurement only (BMC_DEBUG_SKIP=2): no screening, every SAD reads 0
+      for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
+    }
   }
   __syncthreads();
   return g;
@@ -573,6 +577,14 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   const int nt = blockDim.x, nw = nt >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = pc.P * b * b;
+  if (pl.debug & 1) {  // measurement only (BMC_DEBUG_SKIP=1): no selection, report the centre
+    StageResult res;
+    res.dx = cx;
+    res.dy = cy;
+    res.energy = 0.0;
+    res.nvalid = 1;
+    return res;
+  }
   // valid candidates form a rectangle i in [ilo, ihi] x j in [jlo, jhi] (fme.py:250-253)
   const int ilo = max(0, r - floor_div(ox + cx, s)), ihi = min(g.G - 1, r + floor_div(pc.frame_w - b - ox - cx, s));
   const int jlo = max(0, r - floor_div(oy + cy, s)), jhi = min(g.G - 1, r + floor_div(pc.frame_h - b - oy - cy, s));

@@ -25,6 +25,7 @@ struct StagePlan {
   int cur_bytes, win_bytes, tma_bytes;
   int off_sad, off_klist, off_cur, off_win;
   int smem;
+  int debug;      // measurement switches (BMC_DEBUG_SKIP): 1 skip selection, 2 skip screening
 };
 
 #ifndef BMC_STAGE_THREADS
