@@ -234,11 +234,17 @@ int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* 
       std::memset(&a, 0, sizeof a);
       // level 0's first searched stage is centred on (0, 0) for every block: kblk horizontally
       // adjacent blocks share one staged window (fme.py:350-368 with mv = 0 at level 0)
-      a.kblk = (L == 0 && k == 0) ? stage_kblk() : 1;
-      rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, a.kblk);
-      if (rc == BMC_OK && a.kblk > 1 && !a.plan.use_tma) {
+      if (plan_stage_ws(a.plan, *p, b, p->stage_range[s], p->stage_step[s])) {
+        // warp-specialized persistent kernel: screening overlaps staging and selection
         a.kblk = 1;
-        rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, 1);
+        rc = BMC_OK;
+      } else {
+        a.kblk = (L == 0 && k == 0) ? stage_kblk() : 1;
+        rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, a.kblk);
+        if (rc == BMC_OK && a.kblk > 1 && !a.plan.use_tma) {
+          a.kblk = 1;
+          rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, 1);
+        }
       }
       if (rc) return rc;
       a.planes = planes;

@@ -195,6 +195,57 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
   return BMC_OK;
 }
 
+// Plan of the warp-specialized persistent kernel (bmc_fme_ws.cuh): uint8
+// blocks with 4-word chunks, every plane staged in one TMA pass, <= 7
+// screening warps.  Layout: head (+ slot barriers / info), klist, then two slots
+// of {partial sums, current block, window}.
+bool plan_stage_ws(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s) {
+  static const bool off = [] {  // opt-in (BMC_WS=1): measured slower than the classic kernel on C2 (2.99 vs 1.85 ms)
+    const char* e = getenv("BMC_WS");
+    return !(e && *e == '1');
+  }();
+  if (off || p.elem_bytes != 1 || b / 4 < 4) return false;
+  StagePlan q;
+  if (plan_stage(q, p, b, r, s, true, 1) != BMC_OK) return false;
+  if (!q.use_tma || q.pg != p.planes || q.copies || q.threads > 224) return false;  // kWsScreenMax (bmc_fme_ws.cuh)
+  // persistent pipelines only pay off with many blocks per CTA
+  if ((long long)(p.pad_w / b) * (p.pad_h / b) < 4 * 148) return false;
+  const int head = (smem_head_bytes() + 8 * 8 + 2 * 32 + 127) & ~127;  // + slot barriers and infos
+  q.off_klist = head;
+  q.off_sad = q.off_klist + ((2 * q.nmax * 4 + 127) & ~127);
+  q.off_cur = q.off_sad + ((q.parts * q.nmax * 4 + 127) & ~127);
+  q.off_win = q.off_cur + ((q.cur_bytes + 127) & ~127);
+  q.slot_bytes = q.off_win + ((q.win_bytes + 127) & ~127) - q.off_sad;
+  q.smem = q.off_sad + 2 * q.slot_bytes;
+  if (q.smem > kSmemBudget) return false;
+  q.ws = 1;
+  pl = q;
+  return true;
+}
+
+// Dynamic work counters of the WS kernel: a ring of zeroed device words, one
+// per launch (allocated once, outside graph capture).
+unsigned* ws_work_counter(cudaStream_t st) {
+  static std::mutex mu;
+  static unsigned* ring[16] = {};
+  static unsigned next[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!ring[dev]) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return nullptr;
+    if (cudaMalloc(&ring[dev], 256 * sizeof(unsigned)) != cudaSuccess) {
+      ring[dev] = nullptr;
+      return nullptr;
+    }
+  }
+  unsigned* c = ring[dev] + (next[dev]++ % 256);
+  if (cudaMemsetAsync(c, 0, sizeof(unsigned), st) != cudaSuccess) return nullptr;
+  return c;
+}
+
 // Launch one stage.  The TMA maps view a.ref_planes (n_ref_frames frames) for
 // the window and a.planes (n_cur_frames) for the current block.
 int launch_fme_stage(const StageLaunch& a, int n_cur_frames, int n_ref_frames, dim3 grid, cudaStream_t st) {

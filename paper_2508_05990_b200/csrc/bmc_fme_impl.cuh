@@ -335,9 +335,10 @@ __device__ __forceinline__ void sad_run(const uint32_t* rp, const uint32_t* cp, 
 // pass (the item -> thread mapping is identical in every pass).
 template <typename Elem, int CW, int TY, bool SHIFT>
 __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int npl, const StagePlan& pl, int coff_w,
-                          bool add, int nblk) {
+                          bool add, int nblk, int tid0 = -1, int nthr = 0) {
   constexpr int EPW = 4 / sizeof(Elem);
-  const int nt = blockDim.x;
+  const int nt = nthr > 0 ? nthr : (int)blockDim.x;  // the threads taking part (a warp group in the WS kernel)
+  const int t0 = tid0 >= 0 ? tid0 : (int)threadIdx.x;
   const int bww = pl.bw / EPW;
   const int cbw = pl.cbw / EPW;
   const int cpr = (b / EPW) / CW;
@@ -351,7 +352,7 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   const int rstep = s * bww, cstep = s * cbw;
   const int N = g.G * g.G;
   const FastDiv fG(g.G), fncg(g.ncg), frho(nrho), fcpr(cpr), fs(s), fparts(parts);
-  for (int it = threadIdx.x; it < items; it += nt) {
+  for (int it = t0; it < items; it += nt) {
     uint32_t q, i, gi, part, kb;
     fG.divmod(it, q, i);
     fncg.divmod(q, part, gi);
