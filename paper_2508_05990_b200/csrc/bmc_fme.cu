@@ -157,7 +157,11 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
       const int off_win = off_cur + ((cur_bytes + 127) & ~127);
       const int copy_words = (win_bytes / 4 + 31) / 32 * 32 + 8;  // bank skew of 8 words per phase
       const int total = off_win + (want_copies ? (ncopies - 1) * copy_words * 4 + win_bytes : win_bytes);
-      if (total <= kSmemTarget || ((pg == 1 || pg == p.planes) && total <= kSmemBudget)) {
+      static const bool full_planes_big = [] {  // allow all planes staged up to the full budget (1 CTA/SM)
+        const char* e = getenv("BMC_SMEM_SPLIT");
+        return !(e && *e && *e != '0');
+      }();
+      if (total <= kSmemTarget || ((pg == 1 || (pg == p.planes && full_planes_big)) && total <= kSmemBudget)) {
         q.pg = pg;
         q.off_sad = off_sad;
         q.off_klist = off_klist;
