@@ -186,6 +186,19 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     try_plan(alt, false);
     if (alt.pg > pl.pg) pl = alt;
   }
+  {
+    auto magic = [](int d) { return d > 1 ? 0xffffffffu / (uint32_t)d + 1u : 0u; };
+    const int cpr = (b / epw) / cw_words;
+    const int nrho = s < b ? s : b;
+    pl.mG = magic(G);
+    pl.mncg = magic((G + pl.ty - 1) / pl.ty);
+    pl.mrho = magic(nrho);
+    pl.mcpr = magic(cpr);
+    pl.ms = magic(s);
+    pl.mparts = magic(pl.parts);
+    pl.mgw = magic((p.pad_w / b + kblk - 1) / kblk);  // block columns per row of work items
+    pl.per = pl.pg == p.planes ? (p.planes * cpr * nrho + pl.parts - 1) / pl.parts : 0;
+  }
   static const int debug_skip = [] {
     const char* e = getenv("BMC_DEBUG_SKIP");
     return e ? atoi(e) : 0;

@@ -170,6 +170,7 @@ __device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b
 struct FastDiv {
   uint32_t d, m;
   __device__ __forceinline__ explicit FastDiv(uint32_t d_) : d(d_), m(d_ > 1 ? 0xffffffffu / d_ + 1u : 0u) {}
+  __device__ __forceinline__ FastDiv(uint32_t d_, uint32_t m_) : d(d_), m(m_) {}  // host-precomputed magic
   __device__ __forceinline__ uint32_t div(uint32_t n) const { return d > 1 ? __umulhi(n, m) : n; }
   __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
     q = div(n);
@@ -346,12 +347,14 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   const int nrho = s < b ? s : b;  // residue classes of block rows (independent sliding windows)
   const int units = npl * cpr * nrho;
   const int parts = pl.parts;
-  const int per = (units + parts - 1) / parts;
+  const int per = pl.per > 0 ? pl.per : (units + parts - 1) / parts;
   const int cols = g.G * g.ncg;
   const int items = cols * parts * nblk;  // nblk horizontally adjacent blocks share the staged window
   const int rstep = s * bww, cstep = s * cbw;
   const int N = g.G * g.G;
-  const FastDiv fG(g.G), fncg(g.ncg), frho(nrho), fcpr(cpr), fs(s), fparts(parts);
+  // uniform divisors with host-precomputed magics (no integer divide per block)
+  const FastDiv fG(g.G, pl.mG), fncg(g.ncg, pl.mncg), frho(nrho, pl.mrho), fcpr(cpr, pl.mcpr), fs(s, pl.ms),
+      fparts(parts, pl.mparts);
   for (int it = t0; it < items; it += nt) {
     uint32_t q, i, gi, part, kb;
     fG.divmod(it, q, i);
@@ -587,8 +590,10 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     return res;
   }
   // valid candidates form a rectangle i in [ilo, ihi] x j in [jlo, jhi] (fme.py:250-253)
-  const int ilo = max(0, r - floor_div(ox + cx, s)), ihi = min(g.G - 1, r + floor_div(pc.frame_w - b - ox - cx, s));
-  const int jlo = max(0, r - floor_div(oy + cy, s)), jhi = min(g.G - 1, r + floor_div(pc.frame_h - b - oy - cy, s));
+  const FastDiv fsd(s, pl.ms);
+  auto fdiv = [&](int a) { return a >= 0 ? (int)fsd.div(a) : -(int)fsd.div(-a + s - 1); };  // floor(a / s)
+  const int ilo = max(0, r - fdiv(ox + cx)), ihi = min(g.G - 1, r + fdiv(pc.frame_w - b - ox - cx));
+  const int jlo = max(0, r - fdiv(oy + cy)), jhi = min(g.G - 1, r + fdiv(pc.frame_h - b - oy - cy));
   const int wi = ihi - ilo + 1, wj = jhi - jlo + 1;
   StageResult res;
   res.nvalid = (wi > 0 && wj > 0) ? wi * wj : 0;
@@ -598,7 +603,7 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     return res;
   }
 
-  const FastDiv fwi(wi);
+  const FastDiv fwi = wi == g.G ? FastDiv(wi, pl.mG) : FastDiv(wi);  // interior blocks: the full grid width
   // pass 1: fold the parts; first minimum SAD among valid candidates (key = sad<<32 | k)
   unsigned long long best = ~0ull;
   {
@@ -774,8 +779,8 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
       const uint32_t cg = gwg * a.gh;
       pair = (int)(work / cg);
       const int blk = (int)(work - (uint32_t)pair * cg);
-      const int gx0 = (blk % gwg) * a.kblk;
-      gy = blk / gwg;
+      gy = (int)FastDiv(gwg, a.plan.mgw).div(blk);
+      const int gx0 = (blk - gy * (int)gwg) * a.kblk;
       const int nb = min(a.kblk, a.gw - gx0);
       PairCtx<Elem> pc;
       const int cur_f = a.cur_index[pair], ref_f = a.ref_index[pair];
@@ -826,8 +831,8 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
     } else {
       pair = (int)(work / cells);
       const int blk = (int)(work - (uint32_t)pair * cells);
-      gx = blk % a.gw;
-      gy = blk / a.gw;
+      gy = (int)FastDiv(a.gw, a.plan.mgw).div(blk);
+      gx = blk - gy * a.gw;
       cell = (long long)pair * cells + blk;
       ox = gx * b;
       oy = gy * b;
