@@ -187,7 +187,7 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     if (alt.pg > pl.pg) pl = alt;
   }
   {
-    auto magic = [](int d) { return d > 1 ? 0xffffffffu / (uint32_t)d + 1u : 0u; };
+    auto magic = [](int d) { return fastdiv_magic((uint32_t)d); };
     const int cpr = (b / epw) / cw_words;
     const int nrho = s < b ? s : b;
     pl.mG = magic(G);
@@ -197,6 +197,7 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     pl.ms = magic(s);
     pl.mparts = magic(pl.parts);
     pl.mgw = magic((p.pad_w / b + kblk - 1) / kblk);  // block columns per row of work items
+    pl.mcells = magic((p.pad_w / b + kblk - 1) / kblk * (p.pad_h / b));  // work items per frame pair
     pl.per = pl.pg == p.planes ? (p.planes * cpr * nrho + pl.parts - 1) / pl.parts : 0;
   }
   static const int debug_skip = [] {

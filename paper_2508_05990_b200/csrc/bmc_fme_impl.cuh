@@ -165,13 +165,29 @@ struct StageGeom {
 
 __device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
-// Division by a CTA-uniform divisor without the ~20-instruction integer divide:
-// q = umulhi(n, floor(2^32/d) + 1) is exact for n, d < 2^16.
+// Division by a CTA-uniform divisor without the ~20-instruction integer divide
+// (Granlund-Montgomery, exact for every 32-bit numerator): with l = ceil(log2 d)
+// and m = floor(2^32 (2^l - d) / d) + 1,  q = (t + ((n - t) >> 1)) >> (l - 1)
+// where t = umulhi(n, m).  Magics of the uniform divisors are computed on the
+// host (fastdiv_magic); the device constructor is for rare per-block divisors.
+__host__ __device__ inline unsigned long long fastdiv_magic(uint32_t d) {
+  if (d <= 1) return 0ull;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  const unsigned long long m = (((1ull << l) - d) << 32) / d + 1ull;
+  return (m & 0xffffffffull) | ((unsigned long long)l << 32);
+}
+
 struct FastDiv {
-  uint32_t d, m;
-  __device__ __forceinline__ explicit FastDiv(uint32_t d_) : d(d_), m(d_ > 1 ? 0xffffffffu / d_ + 1u : 0u) {}
-  __device__ __forceinline__ FastDiv(uint32_t d_, uint32_t m_) : d(d_), m(m_) {}  // host-precomputed magic
-  __device__ __forceinline__ uint32_t div(uint32_t n) const { return d > 1 ? __umulhi(n, m) : n; }
+  uint32_t d, m, l;
+  __device__ __forceinline__ FastDiv(uint32_t d_, unsigned long long mg) : d(d_), m((uint32_t)mg),
+                                                                             l((uint32_t)(mg >> 32)) {}
+  __device__ __forceinline__ explicit FastDiv(uint32_t d_) : FastDiv(d_, fastdiv_magic(d_)) {}
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    if (d <= 1) return n;
+    const uint32_t t = __umulhi(n, m);
+    return (t + ((n - t) >> 1)) >> (l - 1);
+  }
   __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
     q = div(n);
     r = n - q * d;
@@ -576,6 +592,7 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
 template <typename Elem, int CW, int TY, bool SHIFT>
 __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
                                     const StageGeom& g, uint32_t* sad, int ox, int oy, int b, int coff_e) {
+  const FastDiv fGG(g.G, pl.mG);  // candidate index -> (i, j) without an integer divide
   const int r = g.r, s = g.s, cx = g.cx, cy = g.cy;
   const int N = g.G * g.G;
   const int nt = blockDim.x, nw = nt >> 5;
@@ -638,7 +655,7 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   if (sad0 == 0 && pc.oml > 0.0) {
     // S == 0 gives E == 0.0 exactly; any earlier candidate has S > 0 and,
     // with (1-lam) > 0, E > 0.  The first zero-SAD candidate wins.
-    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, res.dx, res.dy);
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), res.dx, res.dy);
     res.energy = 0.0;
     return res;
   }
@@ -650,8 +667,8 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     double e0 = 0.0;
     if (sad0 != 0) {
       int dx, dy;
-      cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, m0 % g.G, m0 / g.G, dx, dy);
-      e0 = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, m0 % g.G, m0 / g.G, dx, dy);
+      cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), dx, dy);
+      e0 = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), dx, dy);
     }
     if (lane == 0) {
       L.miscd[0] = e0;
@@ -689,7 +706,7 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     const double lim = e0 + kScreenEps;
     for (int e = warp; e < nk; e += nw) {
       const int k = L.klist[e];
-      const int clo = count_lo<Elem>(L, pl, g, pc, ox, oy, b, coff_e, k % g.G, k / g.G, D);
+      const int clo = count_lo<Elem>(L, pl, g, pc, ox, oy, b, coff_e, (int)((k) - fGG.div(k) * g.G), (int)fGG.div(k), D);
       const double elb = __dadd_rn(__dmul_rn(pc.oml, __ddiv_rn((double)sad[k], unit)),
                                    __dmul_rn(pc.lam, __ddiv_rn((double)clo, (double)n)));
       if (lane == 0 && elb - kScreenEps <= lim) L.klist2[atomicAdd(&L.misc[5], 1)] = k;
@@ -703,8 +720,8 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   for (int e = warp; e < nk; e += nw) {
     const int k = rlist[e];
     int dx, dy;
-    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, k % g.G, k / g.G, dx, dy);
-    const double ek = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, k % g.G, k / g.G, dx, dy);
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((k) - fGG.div(k) * g.G), (int)fGG.div(k), dx, dy);
+    const double ek = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, (int)((k) - fGG.div(k) * g.G), (int)fGG.div(k), dx, dy);
     if (ek < be || (ek == be && k < bk)) {
       be = ek;
       bk = k;
@@ -729,7 +746,7 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   }
   __syncthreads();
   const int kw = L.misc[4];
-  cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, kw % g.G, kw / g.G, res.dx, res.dy);
+  cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((kw) - fGG.div(kw) * g.G), (int)fGG.div(kw), res.dx, res.dy);
   res.energy = L.miscd[1];
   return res;
 }
@@ -777,7 +794,7 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
       // nblk horizontally adjacent blocks of level 0's first stage share one window (centre (0, 0))
       const uint32_t gwg = (a.gw + a.kblk - 1) / a.kblk;
       const uint32_t cg = gwg * a.gh;
-      pair = (int)(work / cg);
+      pair = (int)FastDiv(cg, a.plan.mcells).div(work);
       const int blk = (int)(work - (uint32_t)pair * cg);
       gy = (int)FastDiv(gwg, a.plan.mgw).div(blk);
       const int gx0 = (blk - gy * (int)gwg) * a.kblk;
@@ -829,7 +846,7 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
       }
       continue;
     } else {
-      pair = (int)(work / cells);
+      pair = (int)FastDiv(cells, a.plan.mcells).div(work);
       const int blk = (int)(work - (uint32_t)pair * cells);
       gy = (int)FastDiv(a.gw, a.plan.mgw).div(blk);
       gx = blk - gy * a.gw;

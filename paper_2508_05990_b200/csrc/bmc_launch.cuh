@@ -28,8 +28,8 @@ struct StagePlan {
   int debug;      // measurement switches (BMC_DEBUG_SKIP): 1 skip selection, 2 skip screening
   int ws;         // 1: warp-specialized persistent kernel (bmc_fme_ws.cuh), double-buffered slots
   int slot_bytes; // WS: distance between the two slots (sad + cur + win)
-  // host-precomputed fast-division magics (floor(2^32/d)+1) of the CTA-uniform divisors
-  uint32_t mG, mncg, mrho, mcpr, ms, mparts, mgw;
+  // host-precomputed fast-division magics (fastdiv_magic) of the CTA-uniform divisors
+  unsigned long long mG, mncg, mrho, mcpr, ms, mparts, mgw, mcells;
   int per;        // units per part (single-pass plans), 0 = compute on device
 };
 
