@@ -594,7 +594,12 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
         for (int e = 0; e < n; ++e) out[x0 + e] = (uint8_t)(words[e >> 2] >> (8 * (e & 3)));
       }
     }
-    if (t + 1 < t_end) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
+    if (t + 1 < t_end) {
+      // frame t+1 reads labels of frames <= t only when it is not a key frame (in any stream)
+      bool dep = !a.kind;
+      for (int st = 0; st < n_streams && !dep; ++st) dep = a.kind[(long long)st * a.kss + t + 1] != 0;
+      if (dep) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
+    }
   }
 }
 
