@@ -199,6 +199,12 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     pl.mgw = magic((p.pad_w / b + kblk - 1) / kblk);  // block columns per row of work items
     pl.mcells = magic((p.pad_w / b + kblk - 1) / kblk * (p.pad_h / b));  // work items per frame pair
     pl.per = pl.pg == p.planes ? (p.planes * cpr * nrho + pl.parts - 1) / pl.parts : 0;
+    pl.mper = magic(pl.per > 0 ? pl.per : 1);
+    static const bool no_split = [] {
+      const char* e = getenv("BMC_NO_SPLIT");
+      return e && *e && *e != '0';
+    }();
+    pl.split = (!no_split && pl.per > 1) ? 1 : 0;
   }
   static const int debug_skip = [] {
     const char* e = getenv("BMC_DEBUG_SKIP");

@@ -371,7 +371,23 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   // uniform divisors with host-precomputed magics (no integer divide per block)
   const FastDiv fG(g.G, pl.mG), fncg(g.ncg, pl.mncg), frho(nrho, pl.mrho), fcpr(cpr, pl.mcpr), fs(s, pl.ms),
       fparts(parts, pl.mparts);
-  for (int it = t0; it < items; it += nt) {
+  // Items that would only partly fill the last warp are split into one-unit
+  // sub-items (partial sums combined with shared atomics into a pre-zeroed
+  // array), so that warp issues a fraction of a full item's SAD instructions.
+  const int full32 = (items / 32) * 32;
+  // only when the sub-items still fit in the warps the plan launches for the items
+  const bool split = pl.split && !add && full32 + (items - full32) * per <= (items + 31) / 32 * 32;
+  const int n_full = split ? full32 : items;
+  const int n_virt = n_full + (items - n_full) * per;
+  const FastDiv fper(per, pl.mper);
+  for (int vt = t0; vt < n_virt; vt += nt) {
+    int it = vt, sub = -1;
+    if (vt >= n_full) {
+      uint32_t qq, rr;
+      fper.divmod(vt - n_full, qq, rr);
+      it = n_full + (int)qq;
+      sub = (int)rr;
+    }
     uint32_t q, i, gi, part, kb;
     fG.divmod(it, q, i);
     fncg.divmod(q, part, gi);
@@ -383,8 +399,12 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
     uint32_t acc[TY];
 #pragma unroll
     for (int j = 0; j < TY; ++j) acc[j] = 0;
-    const int u_end = min(units, (part + 1) * per);
-    for (int u = part * per; u < u_end; ++u) {
+    int u_beg = part * per, u_end = min(units, (part + 1) * per);
+    if (sub >= 0) {
+      u_beg += sub;
+      u_end = min(u_end, u_beg + 1);
+    }
+    for (int u = u_beg; u < u_end; ++u) {
       uint32_t rho, pc, pp, c;
       frho.divmod(u, pc, rho);
       fcpr.divmod(pc, pp, c);
@@ -401,7 +421,11 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
       const int jj = gi * TY + j;
       if (jj < g.G) {
         const int k = jj * g.G + i;
-        dst[k] = add ? dst[k] + acc[j] : acc[j];
+        if (sub >= 0) {
+          if (u_beg < u_end) atomicAdd(dst + k, acc[j]);
+        } else {
+          dst[k] = add ? dst[k] + acc[j] : acc[j];
+        }
       }
     }
   }
@@ -571,6 +595,8 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
       stage_ldg<Elem>(L, pc.cur + (long long)p0 * pc.plane_stride, pc.ref + (long long)p0 * pc.plane_stride, pc.pitch,
                       pc.plane_stride, pc.frame_h, g, ox, oy, b, npl, pl);
     }
+    if (pl.split && p0 == 0)  // split tail items accumulate with atomics
+      for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
     if (phase_mask & ~1u) {
       __syncthreads();
       build_phase_copies<Elem>(L, pl, npl, phase_mask);

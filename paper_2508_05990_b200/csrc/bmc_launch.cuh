@@ -29,7 +29,8 @@ struct StagePlan {
   int ws;         // 1: warp-specialized persistent kernel (bmc_fme_ws.cuh), double-buffered slots
   int slot_bytes; // WS: distance between the two slots (sad + cur + win)
   // host-precomputed fast-division magics (fastdiv_magic) of the CTA-uniform divisors
-  unsigned long long mG, mncg, mrho, mcpr, ms, mparts, mgw, mcells;
+  unsigned long long mG, mncg, mrho, mcpr, ms, mparts, mgw, mcells, mper;
+  int split;      // split the partial last warp's items into one-unit sub-items (single-pass plans)
   int per;        // units per part (single-pass plans), 0 = compute on device
 };
 
