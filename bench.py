@@ -310,8 +310,9 @@ def run_b200(args, rank, world, local_rank):
     # --- max over ranks (the only collective: one tiny exchange after timing) ---
     from paper_2508_05990_b200 import sharding
     digest = sharding.parity_hash(eng.labels.cpu().numpy(), eng.kind.cpu().numpy())
-    stats = sharding.gather_stats((T - 1) * S * args.steps, total_ms / 1e3, digest, device=dev)
-    vals = torch.tensor([total_ms, statistics.mean(e2e_ms), me_avg], dtype=torch.float64, device=dev)
+    coll_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    stats = sharding.gather_stats((T - 1) * S * args.steps, total_ms / 1e3, digest, device=coll_dev)
+    vals = torch.tensor([total_ms, statistics.mean(e2e_ms), me_avg], dtype=torch.float64, device=coll_dev)
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     total_ms, e2e_avg, me_avg = (float(v) for v in vals.tolist())
@@ -390,17 +391,26 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=1, help="independent clips per GPU (c4: 64 / world)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group for the final timing / parity gather (gloo lets ranks share a GPU in tests)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl != "reference" and args.dist_backend == "gloo":
+        # test mode: several ranks may share one GPU (no NCCL); the hot path has no collective anyway
+        import torch
+        local_rank = local_rank % max(1, torch.cuda.device_count())
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group("gloo")
     try:
         return run_b200(args, rank, world, local_rank)
     finally:
