@@ -146,13 +146,18 @@ int bmc_predict_labels(uint8_t* labels, int64_t frame_stride, int64_t stream_str
  * cooperative launch (frames in order, a grid-wide barrier between them): the
  * batched form of bmc_predict_labels / run_sequence's per-frame
  * predict_labels calls (pipeline.py:123-126).  workspace: one device uint32
- * (barrier counter), reset by the call. */
+ * (barrier counter), reset by the call.  matched (final-level matched flags,
+ * indexed like mv with cells instead of cells*2) + scratch ((n_streams, H, W)
+ * bytes) enable CaBR's weight-free ring-vote refinement of the flagged blocks of
+ * every predicted frame (cabr.refine_blocks with weights=None,
+ * cabr.py:257-345, pipeline.py:127-132); pass NULL for plain prediction. */
 int bmc_predict_labels_clip(uint8_t* labels, int64_t frame_stride, int64_t stream_stride,
                             const uint8_t* key_labels, int n_streams, int t_begin, int t_end,
                             const int32_t* kind, const int32_t* ref, int64_t kind_stream_stride,
                             int height, int width, const int32_t* mv, int64_t mv_frame_stride,
                             int64_t mv_stream_stride, int grid_h, int grid_w, int block_size,
-                            int scale, uint32_t* workspace, void* stream);
+                            int scale, const uint8_t* matched, uint8_t* scratch,
+                            uint32_t* workspace, void* stream);
 
 /* Generalised compensation of a (C, H, W) float32 feature map (bit-exact copy
  * semantics of predict_labels applied per channel). */

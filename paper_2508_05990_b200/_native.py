@@ -72,7 +72,7 @@ _SIGNATURES = {
                                           ctypes.c_int, ctypes.c_int, vp]),
     "bmc_predict_labels_clip": (ctypes.c_int, [vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, i64,
                                                ctypes.c_int, ctypes.c_int, vp, i64, i64, ctypes.c_int, ctypes.c_int,
-                                               ctypes.c_int, ctypes.c_int, vp, vp]),
+                                               ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
     "bmc_predict_features": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]),
 }

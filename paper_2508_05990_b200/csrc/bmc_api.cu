@@ -463,7 +463,7 @@ int bmc_predict_labels_clip(uint8_t* labels, int64_t frame_stride, int64_t strea
                             int n_streams, int t_begin, int t_end, const int32_t* kind, const int32_t* ref,
                             int64_t kind_stream_stride, int height, int width, const int32_t* mv,
                             int64_t mv_frame_stride, int64_t mv_stream_stride, int grid_h, int grid_w, int block_size,
-                            int scale, uint32_t* workspace, void* stream) {
+                            int scale, const uint8_t* matched, uint8_t* scratch, uint32_t* workspace, void* stream) {
   if (!labels || !mv || !kind || !ref || !key_labels || !workspace || n_streams < 0) {
     set_error("NULL argument");
     return BMC_E_ARG;
@@ -496,6 +496,17 @@ int bmc_predict_labels_clip(uint8_t* labels, int64_t frame_stride, int64_t strea
   a.gw = grid_w;
   a.B = B;
   a.scale = scale;
+  if (matched && !scratch) {
+    set_error("ring-vote refinement needs a scratch frame buffer");
+    return BMC_E_ARG;
+  }
+  if (matched && B < 16) {
+    set_error("CaBR block size must be at least 16: the fixed 16x16 context mask would cover a %dx%d block entirely",
+              B, B);
+    return BMC_E_ARG;
+  }
+  a.matched = matched;
+  a.scratch = scratch;
   return launch_predict_chain(a, n_streams, t_begin, t_end, workspace, (cudaStream_t)stream);
 }
 

@@ -106,6 +106,10 @@ struct PredictArgs {
   const int32_t* mv;
   long long mvfs, mvss;
   int gh, gw, B, scale;
+  // CaBR weight-free fallback (ring vote) on the flagged blocks of predicted frames:
+  // flagged = final-level `matched` == 0, same frame / stream indexing as mv (cells, not cells*2)
+  const uint8_t* matched;   // NULL: no refinement
+  uint8_t* scratch;         // (streams, H, W) unrefined prediction of the current frame
 };
 
 int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma, int kblk = 1);

@@ -519,6 +519,68 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
+// CaBR's weight-free fallback (cabr.py:257-345) for frame t: pixels of
+// flagged blocks (final-level matched == 0) take the vote of the ring pixels
+// straight across the four block borders, read from the unrefined prediction
+// in `scratch`; other pixels copy it.  Candidates inside any flagged block are
+// dropped unless all four are; among kept candidates at minimal distance the
+// class with most votes wins, ties to the smallest class id.  All integer.
+__device__ void ring_vote_frame(const PredictArgs& a, int n_streams, int t, long long total, long long per_stream,
+                                int groups_per_row) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
+    const int stream = (int)(g / per_stream);
+    const long long gg = g - stream * per_stream;
+    if (a.kind && a.kind[(long long)stream * a.kss + t] == 0) continue;  // key frames are not refined
+    const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
+    const int n = min(16, a.W - x0);
+    const uint8_t* P = a.scratch + (long long)stream * a.H * a.W;
+    uint8_t* out = a.labels + stream * a.ss + t * a.fs + (long long)y * a.W;
+    const uint8_t* m = a.matched + stream * (a.mvss / 2) + t * (a.mvfs / 2);  // cells per frame / stream
+    const int k = a.B;
+    auto flagged = [&](int py, int px) { return m[(py / k) * a.gw + px / k] == 0; };
+    const int gy = y / k, y0 = gy * k, ly = y - y0;
+    const int ty = min(max(y0 - 1, 0), a.H - 1), by = min(max(y0 + k, 0), a.H - 1);
+    for (int e = 0; e < n; ++e) {
+      const int x = x0 + e;
+      const int gx = x / k;
+      if (m[gy * a.gw + gx] != 0) {
+        out[x] = P[(long long)y * a.W + x];
+        continue;
+      }
+      const int xb = gx * k, lx = x - xb;
+      const int lxp = min(max(xb - 1, 0), a.W - 1), rxp = min(max(xb + k, 0), a.W - 1);
+      const int ry[4] = {ty, by, y, y}, rx[4] = {x, x, lxp, rxp};
+      const int dist[4] = {ly + 1, k - ly, lx + 1, k - lx};
+      int cls[4];
+      bool fl[4], any_clean = false;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        cls[c] = P[(long long)ry[c] * a.W + rx[c]];
+        fl[c] = flagged(ry[c], rx[c]);
+        any_clean |= !fl[c];
+      }
+      int dmin = 0x7fffffff;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (!(any_clean && fl[c])) dmin = min(dmin, dist[c]);
+      int best = 0, best_votes = -1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if ((any_clean && fl[c]) || dist[c] != dmin) continue;
+        int votes = 0;
+#pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2)
+          votes += !(any_clean && fl[c2]) && dist[c2] == dmin && cls[c2] == cls[c];
+        if (votes > best_votes || (votes == best_votes && cls[c] < best)) {
+          best_votes = votes;
+          best = cls[c];
+        }
+      }
+      out[x] = (uint8_t)best;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictArgs a, int n_streams, int t_begin,
                                                                  int t_end, unsigned* barrier_ctr) {
   const int groups_per_row = (a.W + 15) / 16;
@@ -550,6 +612,7 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
       const int r = a.ref ? a.ref[o] : a.ref_fixed;
       const uint8_t* src = a.labels + stream * a.ss + (long long)r * a.fs;
       const int32_t* mv = a.mv + stream * a.mvss + t * a.mvfs;
+      if (a.matched) out = a.scratch + (long long)stream * a.H * a.W + (long long)y * a.W;  // refined below
       const int gy = y / a.B;
       const int gx0 = x0 / a.B, gx1 = (x0 + n - 1) / a.B;
       if (vec_ok && n == 16 && gx0 == gx1) {
@@ -592,6 +655,14 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
         *reinterpret_cast<uint4*>(out + x0) = make_uint4(words[0], words[1], words[2], words[3]);
       } else {
         for (int e = 0; e < n; ++e) out[x0 + e] = (uint8_t)(words[e >> 2] >> (8 * (e & 3)));
+      }
+    }
+    if (a.matched) {
+      bool any_pred = !a.kind;
+      for (int st = 0; st < n_streams && !any_pred; ++st) any_pred = a.kind[(long long)st * a.kss + t] != 0;
+      if (any_pred) {
+        grid_barrier(barrier_ctr, ++epoch * gridDim.x);  // the whole unrefined prediction of frame t is written
+        ring_vote_frame(a, n_streams, t, total, per_stream, groups_per_row);
       }
     }
     if (t + 1 < t_end) {

@@ -98,6 +98,10 @@ class ClipEngine:
         self.Hl, self.Wl = int(h), int(w)
         self.labels = self.torch.zeros((self.S, self.T, h, w), dtype=self.torch.uint8, device=self.dev)
         self.key_labels = self.torch.zeros_like(self.labels)
+        # CaBR weight-free fallback (ring vote) runs inside the label chain when refinement is on
+        self.ring_vote = bool(self.cfg.refine_enabled)
+        self.scratch = self.torch.empty((self.S, h, w), dtype=self.torch.uint8, device=self.dev) \
+            if self.ring_vote else None
         self.graph = None
 
     def load_frames(self, frames, non_blocking: bool = False) -> None:
@@ -190,16 +194,23 @@ class ClipEngine:
             N.ptr(self.cur_index[lo:hi]), N.ptr(self.ref_index[lo:hi]), N.ptr(self.mv_ref[lo:hi]),
             N.ptr(self.e_ref[lo:hi]), N.ptr(self.replaced[lo:hi]), N.stream_handle()))
 
+    def _chain(self, t0: int, t1: int) -> None:
+        """Label chain of frames [t0, t1) of every stream (one cooperative launch); with
+        refine_enabled the flagged blocks of predicted frames get CaBR's ring vote."""
+        cells = self.gh * self.gw
+        cells2 = cells * 2
+        fs = self.Hl * self.Wl
+        ring = self.ring_vote
+        matched = (N.ptr(self.levels[-1].matched) - self.S * cells) if ring else None
+        N.check(N.load().bmc_predict_labels_clip(
+            N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, t0, t1, N.ptr(self.kind),
+            N.ptr(self.ref), self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
+            self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale, matched,
+            N.ptr(self.scratch) if ring else None, N.ptr(self.workspace), N.stream_handle()))
+
     def predict(self) -> None:
         """Label chain (one cooperative launch): key frames copy key_labels, others gather from their reference."""
-        lib = N.load()
-        st = N.stream_handle()
-        cells2 = self.gh * self.gw * 2
-        fs = self.Hl * self.Wl
-        N.check(lib.bmc_predict_labels_clip(
-            N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, 0, self.T, N.ptr(self.kind),
-            N.ptr(self.ref), self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
-            self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale, N.ptr(self.workspace), st))
+        self._chain(0, self.T)
 
     def step(self) -> None:
         self.motion()

@@ -9,10 +9,13 @@ round trip:
      frames (in frame order, as the reference does), uploads them, and
   3. prediction pass: the label chain on device.
 
-Semantics (decisions, labels, ledger) are identical to the reference with
-``refine_enabled=False``.  CaBR-Net block refinement (cabr.py) is the next
-component on the roadmap and is not part of this build, so
-``refine_enabled=True`` raises instead of silently skipping it.
+Semantics (decisions, labels, ledger) are identical to the reference's.  With
+``refine_enabled`` (the default) and no CaBR weights the reference re-labels the
+flagged blocks of every predicted frame with its weight-free ring vote
+(cabr.py:257-345) and the refined labels feed later predictions; the label-chain
+kernel does the same on device.  Running the CaBR-Net forward pass itself
+(``weights`` given) is the next component on the roadmap and raises instead of
+silently skipping it.
 """
 
 from __future__ import annotations
@@ -80,9 +83,9 @@ def run_sequence(frames, key_labels, config: PipelineConfig = PipelineConfig(), 
     if config.refine_enabled and final_block < CABR_MIN_BLOCK:
         raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                          f"{final_block}-pixel blocks; disable refinement or use larger blocks")
-    if config.refine_enabled:
-        raise NotImplementedError("CaBR-Net block refinement is not part of the B200 hot path yet; "
-                                  "run with PipelineConfig(refine_enabled=False)")
+    if config.refine_enabled and weights is not None:
+        raise NotImplementedError("the CaBR-Net forward pass (weights given) is not part of the B200 hot path yet; "
+                                  "pass weights=None for the ring-vote fallback or disable refinement")
     _check_clip(frames)
     planes = 4 if scale == 2 else 1
     backbone = round(config.backbone_gflops * 1e9)
@@ -163,9 +166,10 @@ class ClipSession:
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
                  bayer: bool = True, chunks: int = 6):
-        if config.refine_enabled:
-            raise NotImplementedError("CaBR-Net block refinement is not part of the B200 hot path yet; "
-                                      "run with PipelineConfig(refine_enabled=False)")
+        if config.refine_enabled and config.fme.block_sizes[-1] * (2 if bayer else 1) < CABR_MIN_BLOCK:
+            raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
+                             f"{config.fme.block_sizes[-1] * (2 if bayer else 1)}-pixel blocks; disable refinement "
+                             f"or use larger blocks")
         self.eng = ClipEngine(config, height, width, n_frames, 1, dtype, bayer)
         torch = self.eng.torch
         self.torch = torch
@@ -234,10 +238,7 @@ class ClipSession:
                                                 N.ptr(eng.cur_index[p0:p1]), N.ptr(eng.ref_index[p0:p1]), arr, st))
                 eng._refine(p0, p1)
                 eng._decide(p0 + 1, p1 + 1)
-            N.check(lib.bmc_predict_labels_clip(
-                N.ptr(eng.labels), fs, eng.T * fs, N.ptr(eng.key_labels), eng.S, f0, f1, N.ptr(eng.kind),
-                N.ptr(eng.ref), eng.T, eng.Hl, eng.Wl, N.ptr(eng.mv_ref) - 4 * eng.S * cells2,
-                eng.S * cells2, cells2, eng.gh, eng.gw, eng.b_final, eng.scale, N.ptr(eng.workspace), st))
+            eng._chain(f0, f1)
             ev_out = torch.cuda.Event()
             ev_out.record(cs)
             with torch.cuda.stream(self.copy_out):
@@ -322,10 +323,7 @@ class ClipSession:
         fs = eng.Hl * eng.Wl
         chunks = self.chunks if pipelined else [(0, eng.T)]
         for f0, f1 in chunks:
-            N.check(lib.bmc_predict_labels_clip(
-                N.ptr(eng.labels), fs, eng.T * fs, N.ptr(eng.key_labels), eng.S, f0, f1, N.ptr(eng.kind),
-                N.ptr(eng.ref), eng.T, eng.Hl, eng.Wl, N.ptr(eng.mv_ref) - 4 * eng.S * cells2,
-                eng.S * cells2, cells2, eng.gh, eng.gw, eng.b_final, eng.scale, N.ptr(eng.workspace), st))
+            eng._chain(f0, f1)
             ev = torch.cuda.Event()
             ev.record(cs)
             with torch.cuda.stream(self.copy_out):

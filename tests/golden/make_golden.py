@@ -98,7 +98,8 @@ def pipeline_fixture(name, clip, labels, pcfg, store_inputs=True, inputs_from=No
                         out_labels=np.stack([l.classes for l in res.labels]), kinds=kinds, refs=refs, trig=trig,
                         aem=np.float64(pcfg.aem_threshold), max_gop=np.int64(pcfg.max_gop or 0),
                         has_max_gop=np.bool_(pcfg.max_gop is not None), statistic=np.str_(pcfg.aem_statistic),
-                        policy=np.str_(pcfg.reference_policy), ledger_fme=np.int64(res.ledger["fme"]),
+                        policy=np.str_(pcfg.reference_policy), refine=np.bool_(pcfg.refine_enabled),
+                        ledger_fme=np.int64(res.ledger["fme"]),
                         ledger_refine=np.int64(res.ledger["mv_refine"]), **cfg_arrays(pcfg.fme))
 
 
@@ -122,6 +123,24 @@ def pipeline_fixtures():
                                                            aem_threshold=0.05), **kw)
     pipeline_fixture("c5s_keyframe", clip, lab, PipelineConfig(fme=std, refine_enabled=False,
                                                                reference_policy="keyframe"), **kw)
+
+
+def ringvote_fixtures():
+    # refine_enabled=True without weights: CaBR's ring-vote fallback re-labels the flagged blocks of every
+    # predicted frame and the refined labels feed the next frame's prediction (pipeline.py:123-135)
+    w, h, t = 320, 256, 10
+    clip = synth.bayer_pan_clip(w, h, t, (6, -4), seed=8, square=48, square_velocity=(7, 3))
+    clip[7:] = synth.bayer_pan_clip(w, h, t - 7, (2, 2), seed=99)
+    lab = synth.block_labels(w, h, t)
+    std = fme.get_preset("standard")
+    kw = dict(store_inputs=False, inputs_from="pipe_c5s_default.npz")
+    pipeline_fixture("c5s_ringvote", clip, lab, PipelineConfig(fme=std), **kw)
+    pipeline_fixture("c5s_ringvote_gop4", clip, lab, PipelineConfig(fme=std, max_gop=4, aem_threshold=float("inf")),
+                     **kw)
+    f1 = fme.FmeConfig(stages=(fme.SearchStage(8, 1), fme.SearchStage(0, 1), fme.SearchStage(1, 1)), block_sizes=(16,))
+    c1 = synth.bayer_pan_clip(256, 192, 6, (3, 5), seed=31, square=64, square_velocity=(-5, 3))
+    pipeline_fixture("ringvote_b16_odd", c1, synth.block_labels(256, 192, 6, seed=3),
+                     PipelineConfig(fme=f1, max_gop=6, aem_threshold=float("inf")))
 
 
 def kat_fixtures():
@@ -194,9 +213,16 @@ def decide_fixture():
 
 
 if __name__ == "__main__":
-    me_fixtures()
-    pipeline_fixtures()
-    kat_fixtures()
-    decide_fixture()
+    only = sys.argv[1:]  # e.g. "ringvote": regenerate one group only
+    if not only or "me" in only:
+        me_fixtures()
+    if not only or "pipeline" in only:
+        pipeline_fixtures()
+    if not only or "ringvote" in only:
+        ringvote_fixtures()
+    if not only or "kat" in only:
+        kat_fixtures()
+    if not only or "decide" in only:
+        decide_fixture()
     np.savez_compressed(HERE / "meta.npz", numpy_version=np.str_(np.__version__))
     print("wrote", sorted(p.name for p in HERE.glob("*.npz")))

@@ -47,6 +47,6 @@ def levels(d):
 
 def pipeline_config(d):
     from paper_2508_05990_b200.config import PipelineConfig
-    return PipelineConfig(fme=fme_config(d), refine_enabled=False, aem_threshold=float(d["aem"]),
+    return PipelineConfig(fme=fme_config(d), refine_enabled=bool(d.get("refine", False)), aem_threshold=float(d["aem"]),
                           max_gop=int(d["max_gop"]) if bool(d["has_max_gop"]) else None,
                           aem_statistic=str(d["statistic"]), reference_policy=str(d["policy"]))

@@ -91,7 +91,7 @@ def test_c2_fullsize_identical_frames(cuda, c2_clip):
     assert out.candidate_evals == _valid_area(544, 960, 16, 16) + 2 * 34 * 60
 
 
-@pytest.mark.parametrize("decisions", ["gop4", "threshold"])
+@pytest.mark.parametrize("decisions", ["gop4", "threshold", "gop4_ringvote"])
 def test_c2_fullsize_downstream_stages_match_oracle(cuda, c2_clip, decisions):
     """Whole-clip engine at 1080p: refine, AEM decisions and the label chain are
     checked against the oracle applied to the GPU's own level-0 fields."""
@@ -99,8 +99,9 @@ def test_c2_fullsize_downstream_stages_match_oracle(cuda, c2_clip, decisions):
     from paper_2508_05990_b200.config import PipelineConfig
     from paper_2508_05990_b200.engine import ClipEngine
     T = c2_clip.shape[0]
-    kw = dict(max_gop=4, aem_threshold=float("inf")) if decisions == "gop4" else dict(aem_threshold=0.6)
-    pcfg = PipelineConfig(fme=_c2_cfg(), refine_enabled=False, **kw)
+    kw = dict(max_gop=4, aem_threshold=float("inf")) if decisions.startswith("gop4") else dict(aem_threshold=0.6)
+    ring = decisions.endswith("ringvote")
+    pcfg = PipelineConfig(fme=_c2_cfg(), refine_enabled=ring, **kw)
     labels = synth.block_labels(W, H, T, seed=2)
     eng = ClipEngine(pcfg, H, W, T)
     eng.load_frames(c2_clip)
@@ -128,7 +129,13 @@ def test_c2_fullsize_downstream_stages_match_oracle(cuda, c2_clip, decisions):
                                            max_gop=pcfg.max_gop)
         assert ("key", "nonkey_prev_ref", "nonkey_key_ref")[kinds[t]] == kind
         assert trig[t] == tr
-        out.append(labels[t].classes if kind == "key" else O.predict_labels(out[ref], ref_f, 2))
+        if kind == "key":
+            out.append(labels[t].classes)
+        else:
+            pred = O.predict_labels(out[ref], ref_f, 2)
+            if ring:  # CaBR weight-free fallback on the flagged blocks (32 px = 16 plane px x 2)
+                pred = O.ring_vote_refine(pred, [(gx * 32, gy * 32) for gx, gy in ref_f.refinement_blocks()], 32)
+            out.append(pred)
         np.testing.assert_array_equal(got_labels[t], out[t])
-    if decisions == "gop4":
+    if decisions.startswith("gop4"):
         assert list(kinds) == [0, 1, 1, 1, 0, 1]

@@ -363,7 +363,7 @@ def test_clip_engine_multistream(cuda):
             np.testing.assert_array_equal(got[t], olab[t])
 
 
-@pytest.mark.parametrize("variant", ["callable", "tensor", "gop3", "keyframe"])
+@pytest.mark.parametrize("variant", ["callable", "tensor", "gop3", "keyframe", "ringvote", "ringvote_tensor"])
 def test_clip_session_matches_run_sequence(cuda, variant):
     """The pipelined host-buffer session (chunked H2D / ME / label chain / D2H on three
     streams) returns exactly what run_sequence returns, for both key-label forms."""
@@ -375,15 +375,15 @@ def test_clip_session_matches_run_sequence(cuda, variant):
     clip = synth.bayer_pan_clip(w, h, t, (4, -2), seed=21, square=32, square_velocity=(5, 3))
     labels = synth.block_labels(w, h, t, seed=4)
     fcfg = FmeConfig(stages=(SearchStage(4, 1), SearchStage(0, 1), SearchStage(1, 1)), block_sizes=(16,))
-    kw = dict(fme=fcfg, refine_enabled=False, aem_threshold=0.02)
-    if variant == "gop3":
+    kw = dict(fme=fcfg, refine_enabled=variant.startswith("ringvote"), aem_threshold=0.02)
+    if variant == "gop3" or variant.startswith("ringvote"):
         kw.update(max_gop=3, aem_threshold=float("inf"))
     if variant == "keyframe":
         kw.update(reference_policy="keyframe")
     pcfg = PipelineConfig(**kw)
     ref = run_sequence(synth.frames_of(clip), labels, pcfg)
     sess = ClipSession(pcfg, h, w, t, np.uint8, True, chunks=3)
-    if variant == "tensor":
+    if variant.endswith("tensor"):
         key = cuda.from_numpy(np.stack([l.classes for l in labels])).pin_memory()
     else:
         key = {i: labels[i] for i in range(t)}
@@ -396,3 +396,23 @@ def test_clip_session_matches_run_sequence(cuda, variant):
                 assert refs[i] == d.reference_index
         for i in range(t):
             np.testing.assert_array_equal(got[i], ref.labels[i].classes)
+
+
+def test_ring_vote_pipeline_matches_oracle(cuda):
+    """run_sequence with the default refine_enabled (no CaBR weights): the flagged blocks of every
+    predicted frame take CaBR's ring vote and the refined labels feed later predictions."""
+    from paper_2508_05990_b200 import synth
+    from paper_2508_05990_b200.config import PipelineConfig
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    from paper_2508_05990_b200.pipeline import run_sequence
+    w, h, t = 224, 160, 7
+    clip = synth.bayer_pan_clip(w, h, t, (5, -3), seed=13, square=48, square_velocity=(9, 5))
+    labels = synth.block_labels(w, h, t, seed=9)
+    fcfg = FmeConfig(stages=(SearchStage(3, 1), SearchStage(0, 1), SearchStage(1, 1)), block_sizes=(16, 8))
+    pcfg = PipelineConfig(fme=fcfg, max_gop=5, aem_threshold=float("inf"))
+    res = run_sequence(synth.frames_of(clip), labels, pcfg)
+    olab, odec, _ = O.run_sequence(list(clip), True, [l.classes for l in labels], ocfg(fcfg), pcfg.deviation_threshold,
+                                   pcfg.aem_threshold, pcfg.max_gop, ring_vote=True)
+    assert [d.kind.value for d in res.decisions] == [k for k, _, _ in odec]
+    for i in range(t):
+        np.testing.assert_array_equal(res.labels[i].classes, olab[i])

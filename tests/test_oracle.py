@@ -28,14 +28,14 @@ def test_oracle_matches_golden_me(name):
         assert g.candidate_evals == evals
 
 
-@pytest.mark.parametrize("name", [n for n in G.pipe_fixture_names() if "c1" in n or "default" in n or "gop5" in n
-                                  or "mean" in n or "keyframe" in n])
+@pytest.mark.parametrize("name", G.pipe_fixture_names())
 def test_oracle_matches_golden_pipeline(name):
     d = G.load(name)
     clip, keys = G.pipe_inputs(d)
     pc = G.pipeline_config(d)
     labels, dec, _ = O.run_sequence(list(clip), True, list(keys), G.oracle_cfg(d), pc.deviation_threshold,
-                                    pc.aem_threshold, pc.max_gop, pc.aem_statistic, pc.reference_policy)
+                                    pc.aem_threshold, pc.max_gop, pc.aem_statistic, pc.reference_policy,
+                                    ring_vote=pc.refine_enabled)
     codes = {"key": 0, "nonkey_prev_ref": 1, "nonkey_key_ref": 2}
     np.testing.assert_array_equal([codes[k] for k, _, _ in dec], d["kinds"])
     np.testing.assert_array_equal([-1 if r is None else r for _, r, _ in dec], d["refs"])
