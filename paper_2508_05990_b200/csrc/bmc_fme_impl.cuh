@@ -667,17 +667,15 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   }
   if (lane == 0) L.red64[warp] = best;
   __syncthreads();
+  // every thread folds the per-warp minima itself (no serial step, no second barrier)
+  unsigned long long b0 = L.red64[0];
+  for (int w = 1; w < nw; ++w) b0 = L.red64[w] < b0 ? L.red64[w] : b0;
   if (tid == 0) {
-    unsigned long long b0 = L.red64[0];
-    for (int w = 1; w < nw; ++w) b0 = L.red64[w] < b0 ? L.red64[w] : b0;
-    L.misc[0] = (int)(b0 & 0xffffffffu);
-    L.misc[2] = (int)(b0 >> 32);
-    L.misc[3] = 0;  // klist size
+    L.misc[3] = 0;  // klist size   (ordered before use by the barrier after the table fill)
     L.misc[5] = 0;  // replay list size
   }
-  __syncthreads();
-  const int m0 = L.misc[0];
-  const unsigned sad0 = (unsigned)L.misc[2];
+  const int m0 = (int)(b0 & 0xffffffffu);
+  const unsigned sad0 = (unsigned)(b0 >> 32);
   if (sad0 == 0 && pc.oml > 0.0) {
     // S == 0 gives E == 0.0 exactly; any earlier candidate has S > 0 and,
     // with (1-lam) > 0, E > 0.  The first zero-SAD candidate wins.
