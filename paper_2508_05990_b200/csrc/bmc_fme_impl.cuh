@@ -580,6 +580,24 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
     for (int i = 0; i < min(g.G, EPW); ++i) phase_mask |= 1u << ((g.d + i * s) % EPW);
 
   __syncthreads();  // previous users of smem are done; mbarrier init visible
+  if (pl.use_tma && pl.pg == pc.P && !(phase_mask & ~1u) && !(pl.debug & 2)) {
+    // common case, one TMA pass: clear the atomic-accumulated sums while the
+    // boxes are in flight; each thread's mbarrier wait then makes the staged
+    // tiles visible to it, so no CTA barrier is needed after the wait
+    if (tid == 0) {
+      mbar_expect_tx(L.bar, (uint32_t)(pl.tma_bytes));  // full boxes, OOB included
+      tma_load_3d(L.win, tm_win, g.tx0, g.wy0, pc.ref_z, L.bar);
+      tma_load_3d(L.cur, tm_cur, cx0, oy, pc.cur_z, L.bar);
+    }
+    if (pl.split)
+      for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
+    __syncthreads();
+    mbar_wait(L.bar, phase);
+    phase ^= 1;
+    sad_items<Elem, CW, TY, SHIFT>(L, g, b, pc.P, pl, coff_w, false, nblk);
+    __syncthreads();
+    return g;
+  }
   for (int p0 = 0; p0 < pc.P; p0 += pl.pg) {
     const int npl = min(pl.pg, pc.P - p0);
     if (p0) __syncthreads();
