@@ -730,11 +730,27 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   __syncthreads();
   const double e0 = L.miscd[0];
   const unsigned sthr = (unsigned)L.misc[6];
-  // pass 2: SAD contenders (candidates whose lower bound reaches e0)
-  for (int v = tid; v < res.nvalid; v += nt) {
-    const int jv = fwi.div(v);
-    const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
-    if (k != m0 && sad[k] <= sthr) L.klist[atomicAdd(&L.misc[3], 1)] = k;
+  // pass 2: SAD contenders (candidates whose lower bound reaches e0).  A
+  // sample that does not count contributes at most D-1 to S and one that counts
+  // at most s, so C >= (S - (D-1) n) / (s - D + 1): a free sparsity bound that
+  // prunes poor candidates before any count_lo / float64 work.
+  {
+    const int Dc = (int)floor(pc.tol * (double)pc.max_value + 1e-9) + 1;
+    const long long slack = (long long)(Dc - 1) * n;
+    const int span = pc.max_value - Dc + 1;
+    const double lim2 = e0 + kScreenEps;
+    for (int v = tid; v < res.nvalid; v += nt) {
+      const int jv = fwi.div(v);
+      const int k = (jlo + jv) * g.G + ilo + (v - jv * wi);
+      if (k == m0 || sad[k] > sthr) continue;
+      if (pc.lam > 0.0 && span > 0 && (long long)sad[k] > slack) {
+        const long long cl = ((long long)sad[k] - slack + span - 1) / span;
+        const double elb = __dadd_rn(__dmul_rn(pc.oml, __ddiv_rn((double)sad[k], unit)),
+                                     __dmul_rn(pc.lam, __ddiv_rn((double)cl, (double)n)));
+        if (elb - kScreenEps > lim2) continue;
+      }
+      L.klist[atomicAdd(&L.misc[3], 1)] = k;
+    }
   }
   __syncthreads();
   int nk = L.misc[3];
