@@ -40,6 +40,8 @@ CONFIGS = {
     # name: (W, H, T, velocity, seed, stages, block_sizes, dtype, description)
     "c2": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
            "1920x1080 RGGB uint8 30-frame pan clip, 16x16 blocks, +-16 full search, AEM key selection"),
+    "c2u16": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint16",
+              "1920x1080 RGGB uint16 30-frame pan clip (C2's uint16 variant), 16x16 blocks, +-16 full search"),
     "c1": (256, 256, 8, (2, 2), 3, ((8, 1), (0, 1), (0, 1)), (16,), "uint8",
            "256x256 RGGB uint8 8-frame clip, 16x16 blocks, +-8 full search"),
     "c3": (3840, 2160, 60, (6, -4), 11, ((4, 8), (2, 4), (2, 1)), (8,), "uint16",
