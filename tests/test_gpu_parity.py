@@ -416,3 +416,32 @@ def test_ring_vote_pipeline_matches_oracle(cuda):
     assert [d.kind.value for d in res.decisions] == [k for k, _, _ in odec]
     for i in range(t):
         np.testing.assert_array_equal(res.labels[i].classes, olab[i])
+
+
+@pytest.mark.parametrize("policy", ["previous", "keyframe"])
+def test_multistream_engine_ring_vote(cuda, policy):
+    """Three streams in one engine with CaBR's ring vote in the label chain == the oracle per stream."""
+    from paper_2508_05990_b200 import synth
+    from paper_2508_05990_b200.config import PipelineConfig
+    from paper_2508_05990_b200.engine import ClipEngine
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    fcfg = FmeConfig(stages=(SearchStage(3, 1), SearchStage(0, 1), SearchStage(1, 1)), block_sizes=(16,))
+    pcfg = PipelineConfig(fme=fcfg, max_gop=4, aem_threshold=float("inf"), reference_policy=policy)
+    S, T, h, w = 3, 6, 128, 160
+    clips = np.stack([synth.bayer_pan_clip(w, h, T, (2 * s + 1, -3), seed=70 + s, square=32,
+                                           square_velocity=(5, 2 * s)) for s in range(S)])
+    eng = ClipEngine(pcfg, h, w, T, S)
+    eng.load_frames(clips)
+    labels = [synth.block_labels(w, h, T, seed=s) for s in range(S)]
+    for s in range(S):
+        for t in range(T):
+            eng.key_labels[s, t].copy_(cuda.from_numpy(labels[s][t].classes.copy()))
+    eng.step()
+    cuda.cuda.synchronize()
+    for s in range(S):
+        olab, _, _ = O.run_sequence(list(clips[s]), True, [l.classes for l in labels[s]], ocfg(fcfg),
+                                    pcfg.deviation_threshold, pcfg.aem_threshold, pcfg.max_gop,
+                                    reference_policy=policy, ring_vote=True)
+        got = eng.labels[s].cpu().numpy()
+        for t in range(T):
+            np.testing.assert_array_equal(got[t], olab[t])
