@@ -147,24 +147,24 @@ __device__ __forceinline__ int lower_median(int* v, int n) {
 
 template <typename Elem>
 __global__ void __launch_bounds__(kThreads) refine_kernel(const RefineArgs a) {
+  // Phase 1: one thread per block (clipped 3x3 window of the INPUT field, lower-middle
+  // medians, Chebyshev test).  Phase 2: the CTA's replaced blocks whose new window is
+  // in frame re-evaluate their energy, one warp per block (exact float64 replay).
   __shared__ double tab8[256];
+  __shared__ int todo[kThreads];
+  __shared__ int ntodo;
   const bmc_fme_params& p = a.prm;
   const double* tab = a.tab16;
-  if (sizeof(Elem) == 1) {
-    for (int v = threadIdx.x; v < 256; v += blockDim.x) tab8[v] = __ddiv_rn((double)v, (double)p.max_value);
-    tab = tab8;
-  }
+  const long long per_pair = (long long)a.gh * a.gw;
+  const long long cells = (long long)a.n_pairs * per_pair;
+  const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0) ntodo = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const long long cells = (long long)a.n_pairs * a.gh * a.gw;
-  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (wid >= cells) return;
-  const int pair = (int)(wid / ((long long)a.gh * a.gw));
-  const int cell = (int)(wid % ((long long)a.gh * a.gw));
-  const int gy = cell / a.gw, gx = cell % a.gw;
-  const int32_t* mv = a.mv_in + (long long)pair * a.gh * a.gw * 2;
-  int mx = 0, my = 0, rep = 0;
-  if (lane == 0) {
+  if (o < cells) {
+    const int pair = (int)(o / per_pair);
+    const int cell = (int)(o - pair * per_pair);
+    const int gy = cell / a.gw, gx = cell - (cell / a.gw) * a.gw;
+    const int32_t* mv = a.mv_in + (long long)pair * per_pair * 2;
     int vx[9], vy[9], n = 0;
     for (int y = max(0, gy - 1); y < min(a.gh, gy + 2); ++y)
       for (int x = max(0, gx - 1); x < min(a.gw, gx + 2); ++x) {
@@ -173,43 +173,51 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(const RefineArgs a) {
         ++n;
       }
     const int medx = lower_median(vx, n), medy = lower_median(vy, n);
-    mx = mv[2 * cell];
-    my = mv[2 * cell + 1];
-    const int dev = max(abs(mx - medx), abs(my - medy));
-    if (dev > a.thr) {
+    int mx = mv[2 * cell], my = mv[2 * cell + 1], rep = 0;
+    if (max(abs(mx - medx), abs(my - medy)) > a.thr) {
       mx = medx;
       my = medy;
       rep = 1;
     }
-  }
-  mx = __shfl_sync(0xffffffffu, mx, 0);
-  my = __shfl_sync(0xffffffffu, my, 0);
-  rep = __shfl_sync(0xffffffffu, rep, 0);
-  const long long o = (long long)pair * a.gh * a.gw + cell;
-  double e = a.e_in[o];
-  if (rep && a.planes) {
-    const int ox = gx * a.b, oy = gy * a.b;
-    const int rx = ox + mx, ry = oy + my;
-    if (rx >= 0 && rx <= p.pad_w - a.b && ry >= 0 && ry <= p.pad_h - a.b) {  // mv_refine.py:60
-      const Elem* base = reinterpret_cast<const Elem*>(a.planes);
-      const Elem* cur = base + (long long)a.cur_index[pair] * p.frame_stride + (long long)oy * p.pitch + ox;
-      const Elem* ref = base + (long long)a.ref_index[pair] * p.frame_stride + (long long)ry * p.pitch + rx;
-      e = exact_energy_warp<Elem>(cur, ref, p.pitch, p.plane_stride, a.b, p.planes, tab, p.sparsity_tolerance,
-                                  p.one_minus_lam, p.lam)
-              .energy;
-    }
-  }
-  if (lane == 0) {
     a.mv_out[2 * o] = mx;
     a.mv_out[2 * o + 1] = my;
-    a.e_out[o] = e;
+    a.e_out[o] = a.e_in[o];
     if (a.replaced) a.replaced[o] = rep;
+    if (rep && a.planes) {
+      const int rx = gx * a.b + mx, ry = gy * a.b + my;
+      if (rx >= 0 && rx <= p.pad_w - a.b && ry >= 0 && ry <= p.pad_h - a.b)  // mv_refine.py:60
+        todo[atomicAdd(&ntodo, 1)] = (int)threadIdx.x;
+    }
+  }
+  __syncthreads();
+  const int nt = ntodo;
+  if (nt == 0) return;
+  if (sizeof(Elem) == 1) {
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) tab8[v] = __ddiv_rn((double)v, (double)p.max_value);
+    tab = tab8;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = warp; e < nt; e += blockDim.x >> 5) {
+    const long long oo = blockIdx.x * (long long)blockDim.x + todo[e];
+    const int pair = (int)(oo / per_pair);
+    const int cell = (int)(oo - pair * per_pair);
+    const int gy = cell / a.gw, gx = cell - (cell / a.gw) * a.gw;
+    const int mx = a.mv_out[2 * oo], my = a.mv_out[2 * oo + 1];
+    const int ox = gx * a.b, oy = gy * a.b;
+    const Elem* base = reinterpret_cast<const Elem*>(a.planes);
+    const Elem* cur = base + (long long)a.cur_index[pair] * p.frame_stride + (long long)oy * p.pitch + ox;
+    const Elem* ref = base + (long long)a.ref_index[pair] * p.frame_stride + (long long)(oy + my) * p.pitch + ox + mx;
+    const double en = exact_energy_warp<Elem>(cur, ref, p.pitch, p.plane_stride, a.b, p.planes, tab,
+                                              p.sparsity_tolerance, p.one_minus_lam, p.lam)
+                          .energy;
+    if (lane == 0) a.e_out[oo] = en;
   }
 }
 
 int launch_refine(const RefineArgs& a, cudaStream_t st) {
-  const long long warps = (long long)a.n_pairs * a.gh * a.gw;
-  const long long blocks = (warps * 32 + kThreads - 1) / kThreads;
+  const long long cells = (long long)a.n_pairs * a.gh * a.gw;
+  const long long blocks = (cells + kThreads - 1) / kThreads;
   if (a.prm.elem_bytes == 1)
     refine_kernel<uint8_t><<<(unsigned)blocks, kThreads, 0, st>>>(a);
   else
