@@ -62,7 +62,7 @@ constexpr int kMaxSW = ((kMaxStageThreads + 31) / 32 + 1) / 2 * 2;  // warps per
 // ---------------------------------------------------------------------------
 struct SmemLayout {
   double* tab;                 // fl(v/255) for uint8
-  unsigned long long* red64;   // [kMaxSW]
+  unsigned long long* red64;   // [2][kMaxSW] (alternating per block of a kblk set)
   double* best_e;              // [kMaxSW]
   int* best_k;                 // [kMaxSW]
   int* misc;                   // [16]
@@ -80,7 +80,7 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   L.tab = reinterpret_cast<double*>(base);
   unsigned char* p = base + 256 * sizeof(double);
   L.red64 = reinterpret_cast<unsigned long long*>(p);
-  p += kMaxSW * 8;
+  p += 2 * kMaxSW * 8;
   L.best_e = reinterpret_cast<double*>(p);
   p += kMaxSW * 8;
   L.best_k = reinterpret_cast<int*>(p);
@@ -98,7 +98,7 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   return L;
 }
 
-static inline int smem_head_bytes() { return 256 * 8 + kMaxSW * 20 + 16 * 4 + 4 * 8 + 16; }
+static inline int smem_head_bytes() { return 256 * 8 + kMaxSW * 28 + 16 * 4 + 4 * 8 + 16; }
 
 // ---------------------------------------------------------------------------
 // TMA helpers (inline PTX)
@@ -380,6 +380,7 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
   const int n_full = split ? full32 : items;
   const int n_virt = n_full + (items - n_full) * per;
   const FastDiv fper(per, pl.mper);
+  const bool unit_is_plane = (s == 1 && cpr == 1);  // full-search stages: one unit per plane, all b rows
   for (int vt = t0; vt < n_virt; vt += nt) {
     int it = vt, sub = -1;
     if (vt >= n_full) {
@@ -405,14 +406,16 @@ __device__ void sad_items(const SmemLayout& L, const StageGeom& g, int b, int np
       u_end = min(u_end, u_beg + 1);
     }
     for (int u = u_beg; u < u_end; ++u) {
-      uint32_t rho, pc, pp, c;
-      frho.divmod(u, pc, rho);
-      fcpr.divmod(pc, pp, c);
+      uint32_t rho = 0, pc, pp = (uint32_t)u, c = 0;
+      if (!unit_is_plane) {
+        frho.divmod(u, pc, rho);
+        fcpr.divmod(pc, pp, c);
+      }
       // window rows past hwin (next plane / slack rows) only feed the padding
       // candidates of the last row group, whose sums are discarded.
       const uint32_t* R0 = win + pp * pl.wrows * bww + (xo / EPW) + c * CW;
       const uint32_t* C0 = L.cur + pp * b * cbw + coff_w + kb * (b / EPW) + c * CW;
-      const int M = (int)fs.div(b - 1 - rho) + 1;
+      const int M = unit_is_plane ? b : (int)fs.div(b - 1 - rho) + 1;
       sad_run<Elem, CW, TY, SHIFT>(R0 + (rho + gi * TY * s) * bww, C0 + rho * cbw, rstep, cstep, M, sh, acc);
     }
     uint32_t* dst = L.sad + (kb * parts + part) * N;
@@ -635,7 +638,8 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
 // All threads participate and receive the result.
 template <typename Elem, int CW, int TY, bool SHIFT>
 __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc, const StagePlan& pl,
-                                    const StageGeom& g, uint32_t* sad, int ox, int oy, int b, int coff_e) {
+                                    const StageGeom& g, uint32_t* sad, int ox, int oy, int b, int coff_e,
+                                    int slot = 0) {
   const FastDiv fGG(g.G, pl.mG);  // candidate index -> (i, j) without an integer divide
   const int r = g.r, s = g.s, cx = g.cx, cy = g.cy;
   const int N = g.G * g.G;
@@ -683,11 +687,15 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, m);
     best = o < best ? o : best;
   }
-  if (lane == 0) L.red64[warp] = best;
+  // consecutive blocks of a kblk set alternate halves of red64: the zero-SAD
+  // exit below has no trailing barrier, so a fast warp's next write must not
+  // land in the half a slower warp may still be folding
+  unsigned long long* red = L.red64 + (slot & 1) * kMaxSW;
+  if (lane == 0) red[warp] = best;
   __syncthreads();
   // every thread folds the per-warp minima itself (no serial step, no second barrier)
-  unsigned long long b0 = L.red64[0];
-  for (int w = 1; w < nw; ++w) b0 = L.red64[w] < b0 ? L.red64[w] : b0;
+  unsigned long long b0 = red[0];
+  for (int w = 1; w < nw; ++w) b0 = red[w] < b0 ? red[w] : b0;
   if (tid == 0) {
     L.misc[3] = 0;  // klist size   (ordered before use by the barrier after the table fill)
     L.misc[5] = 0;  // replay list size
@@ -838,9 +846,7 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
   // over the (pair, block) work list, so the prologue and the per-stage
   // constants are paid once per CTA, not once per block.
   const uint32_t cells = (uint32_t)a.gw * a.gh;
-  const uint32_t total = a.single ? 1u
-                                  : (uint32_t)((a.gw + a.kblk - 1) / a.kblk) * a.gh * (uint32_t)a.n_pairs;
-  for (uint32_t work = blockIdx.x; work < total; work += gridDim.x) {
+  for (uint32_t work = blockIdx.x; work < a.total; work += gridDim.x) {
     int pair = 0, gx = 0, gy = 0, ox, oy, sx = 0, sy = 0;
     long long cell = 0;
     if (a.single) {
@@ -850,7 +856,7 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
       sy = a.cy;
     } else if (a.kblk > 1) {
       // nblk horizontally adjacent blocks of level 0's first stage share one window (centre (0, 0))
-      const uint32_t gwg = (a.gw + a.kblk - 1) / a.kblk;
+      const uint32_t gwg = a.gwg;
       const uint32_t cg = gwg * a.gh;
       pair = (int)FastDiv(cg, a.plan.mcells).div(work);
       const int blk = (int)(work - (uint32_t)pair * cg);
@@ -883,7 +889,7 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
         StageGeom gk = g;
         gk.d += kb * b;
         const StageResult res = select_block<Elem, CW, TY, SHIFT>(L, pc, a.plan, gk, L.sad + kb * nsad, ox0 + kb * b,
-                                                                  oy, b, coff_e + kb * b);
+                                                                  oy, b, coff_e + kb * b, kb);
         if (threadIdx.x == 0) {
           const long long c = (long long)pair * cells + (long long)gy * a.gw + gx0 + kb;
           a.mv[2 * c] = res.dx;
@@ -1022,6 +1028,9 @@ template <typename E, int CW, int TY, bool SH>
 inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid, cudaStream_t st) {
   int rc = set_smem(fme_stage_kernel<E, CW, TY, SH>, a.plan.smem);
   if (rc) return rc;
+  StageLaunch la = a;
+  la.gwg = (uint32_t)((a.gw + a.kblk - 1) / a.kblk);
+  la.total = a.single ? 1u : la.gwg * (uint32_t)a.gh * (uint32_t)a.n_pairs;
   static const bool plan_log = [] {
     const char* e = getenv("BMC_PLAN_LOG");
     return e && *e && *e != '0';
@@ -1070,7 +1079,7 @@ inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageL
   }();
   const long long capacity = persist_mult > 0 ? (long long)per_sm * sms * persist_mult : work;
   const unsigned nblk = (unsigned)(work < capacity ? work : capacity);
-  fme_stage_kernel<E, CW, TY, SH><<<nblk, a.plan.threads, a.plan.smem, st>>>(tw, tc, a);
+  fme_stage_kernel<E, CW, TY, SH><<<nblk, a.plan.threads, a.plan.smem, st>>>(tw, tc, la);
   rc = cuda_status(cudaGetLastError(), "fme_stage_kernel");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (!rc && sync_debug() && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {

@@ -62,6 +62,7 @@ struct StageLaunch {
   int single;               // search_stage API: one block at (ox, oy), centre (cx, cy)
   int ox, oy, cx, cy;
   int32_t* nvalid_out;
+  uint32_t gwg, total;      // set by the launcher: work items per block row / per launch
 };
 
 struct RefineArgs {

@@ -165,7 +165,7 @@ class ClipSession:
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True, chunks: int = 6):
+                 bayer: bool = True, chunks: int = 10):
         if config.refine_enabled and config.fme.block_sizes[-1] * (2 if bayer else 1) < CABR_MIN_BLOCK:
             raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                              f"{config.fme.block_sizes[-1] * (2 if bayer else 1)}-pixel blocks; disable refinement "

@@ -10,7 +10,7 @@ for spec in "$@"; do
   timeout 600 env $PROF_ENV ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-fme_} -s $skip -c 1 -o $rep \
       python tools/prof_me.py $cfg 1 > $rep.log 2>&1
   python tools/ncu_summary.py $rep.ncu-rep > $rep.txt 2>&1
-  python tools/ncu_lines.py $rep.ncu-rep 25 >> $rep.txt 2>&1
+  python tools/ncu_lines.py $rep.ncu-rep ${NLINES:-25} >> $rep.txt 2>&1
   ncu -i $rep.ncu-rep --page details --csv 2>/dev/null | grep -E '"(Duration|Registers Per Thread|Achieved Occupancy|Theoretical Occupancy|Block Limit [A-Za-z ]+|Grid Size|Block Size|Dynamic Shared Memory Per Block)"' | cut -d, -f5- >> $rep.txt
   python tools/ncu_sass_counts.py $rep.ncu-rep > $rep.sass.tsv 2>&1
   rm -f $rep.ncu-rep
