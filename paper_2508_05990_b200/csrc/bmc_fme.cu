@@ -106,6 +106,42 @@ static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed, i
   pl.threads = best_threads;
 }
 
+// Average shared-memory wavefronts per reference-row load of the screening
+// loop (sad_items' item -> lane mapping, one warp step at block row 0) for a
+// window row stride of bww words.  Lanes of neighbouring TY-row groups read rows
+// TY*s apart, so a stride with TY*s*bww = 8 (mod 32) puts the two groups'
+// ~9-word column spans on the same banks.
+static double row_load_wavefronts(const StagePlan& pl, int bww, int G, int b, int s, int kblk, int epw, int cw,
+                                  int units) {
+  const int ncg = (G + pl.ty - 1) / pl.ty;
+  const int items = G * ncg * pl.parts * kblk;
+  const int per = (units + pl.parts - 1) / pl.parts;
+  const int wpl = units / (pl.pg > 0 ? pl.pg : 1);  // units per plane
+  long long tot = 0, n = 0;
+  for (int w0 = 0; w0 + 32 <= items; w0 += 32) {
+    for (int qw = 0; qw <= cw; ++qw) {
+      int bank_cnt[32] = {0};
+      int addrs[32][32];
+      for (int l = 0; l < 32; ++l) {
+        const int it = w0 + l;
+        const int i = it % G, q = it / G;
+        const int gi = q % ncg, part = (q / ncg) % pl.parts, kb = (q / ncg) / pl.parts;
+        const int plane = wpl > 0 ? (part * per) / wpl : 0;
+        const long long addr = (long long)(plane * pl.wrows + gi * pl.ty * s) * bww + (kb * b + i * s) / epw + qw;
+        const int bank = (int)(addr % 32);
+        bool seen = false;
+        for (int k = 0; k < bank_cnt[bank]; ++k) seen |= addrs[bank][k] == (int)addr;
+        if (!seen && bank_cnt[bank] < 32) addrs[bank][bank_cnt[bank]++] = (int)addr;
+      }
+      int mx = 1;
+      for (int k = 0; k < 32; ++k) mx = bank_cnt[k] > mx ? bank_cnt[k] : mx;
+      tot += mx;
+      ++n;
+    }
+  }
+  return n ? (double)tot / n : 1.0;
+}
+
 int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma, int kblk) {
   std::memset(&pl, 0, sizeof pl);
   const int eb = p.elem_bytes, epw = 4 / eb;
@@ -185,6 +221,38 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     StagePlan alt = pl;
     try_plan(alt, false);
     if (alt.pg > pl.pg) pl = alt;
+  }
+  static const bool no_pitch = [] {
+    const char* e = getenv("BMC_NO_PITCH");
+    return e && *e && *e != '0';
+  }();
+  if (pl.pg && pl.use_tma && !pl.copies && !no_pitch) {
+    // widen the TMA box (= the smem row stride) by up to two 16-byte steps when
+    // that removes bank conflicts on the screening loop's row loads, as long as
+    // the SM still holds as many CTAs
+    const int units = pl.pg * chunks * (s < b ? s : b);
+    const double base = row_load_wavefronts(pl, pl.bw / epw, G, b, s, kblk, epw, cw_words, units);
+    const int ctas0 = (228 * 1024) / (pl.smem + 1024);
+    int best_bw = pl.bw;
+    double best_wf = base;
+    for (int k = 1; k <= 2; ++k) {
+      const int bw2 = pl.bw + k * align;
+      if (bw2 > 256) break;
+      const int grow = (pl.pg * pl.wrows + pl.ty * s) * (bw2 - pl.bw) * eb;
+      if ((228 * 1024) / (pl.smem + grow + 1024) < (ctas0 < 4 ? ctas0 : 4)) break;
+      const double wf = row_load_wavefronts(pl, bw2 / epw, G, b, s, kblk, epw, cw_words, units);
+      if (wf < best_wf - 0.05) {
+        best_wf = wf;
+        best_bw = bw2;
+      }
+    }
+    if (best_bw != pl.bw) {
+      const int grow = (pl.pg * pl.wrows + pl.ty * s) * (best_bw - pl.bw) * eb;
+      pl.win_bytes += grow;
+      pl.smem += grow;
+      pl.tma_bytes += pl.pg * pl.hwin * (best_bw - pl.bw) * eb;
+      pl.bw = best_bw;
+    }
   }
   {
     auto magic = [](int d) { return fastdiv_magic((uint32_t)d); };
