@@ -13,5 +13,6 @@ for spec in "$@"; do
   python tools/ncu_lines.py $rep.ncu-rep ${NLINES:-25} >> $rep.txt 2>&1
   ncu -i $rep.ncu-rep --page details --csv 2>/dev/null | grep -E '"(Duration|Registers Per Thread|Achieved Occupancy|Theoretical Occupancy|Block Limit [A-Za-z ]+|Grid Size|Block Size|Dynamic Shared Memory Per Block)"' | cut -d, -f5- >> $rep.txt
   python tools/ncu_sass_counts.py $rep.ncu-rep > $rep.sass.tsv 2>&1
+  python tools/ncu_smem_conf.py $rep.ncu-rep > $rep.smem.txt 2>&1
   rm -f $rep.ncu-rep
 done
