@@ -589,96 +589,160 @@ __device__ void ring_vote_frame(const PredictArgs& a, int n_streams, int t, long
   }
 }
 
+// Gather of one 16-pixel group of a non-key frame t of one stream
+// (propagate.py:39-53): out[y, x] = ref[clip(y + s*dy), clip(x + s*dx)].
+__device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int stream, int t, long long o, int y, int x0,
+                                                   bool vec_ok) {
+  uint8_t* out = a.labels + stream * a.ss + t * a.fs + (long long)y * a.W;
+  const int n = min(16, a.W - x0);
+  const int r = a.ref ? a.ref[o] : a.ref_fixed;
+  const uint8_t* src = a.labels + stream * a.ss + (long long)r * a.fs;
+  const int32_t* mv = a.mv + stream * a.mvss + t * a.mvfs;
+  if (a.matched) out = a.scratch + (long long)stream * a.H * a.W + (long long)y * a.W;  // refined below
+  const int gy = y / a.B;
+  const int gx0 = x0 / a.B, gx1 = (x0 + n - 1) / a.B;
+  if (vec_ok && n == 16 && gx0 == gx1) {
+    const int c = gy * a.gw + gx0;
+    const int dx = __ldg(mv + 2 * c) * a.scale, dy = __ldg(mv + 2 * c + 1) * a.scale;
+    const int sy = min(max(y + dy, 0), a.H - 1);
+    const int sx = x0 + dx;
+    if (sx >= 0 && sx + 16 <= a.W) {
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(src + (long long)sy * a.W);
+      const int w0 = sx >> 2, sh = (sx & 3) * 8;
+      uint32_t v[5];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcg(row + w0 + q);
+      v[4] = sh ? __ldcg(row + w0 + 4) : 0u;
+      uint4 o4;
+      o4.x = __funnelshift_r(v[0], v[1], sh);
+      o4.y = __funnelshift_r(v[1], v[2], sh);
+      o4.z = __funnelshift_r(v[2], v[3], sh);
+      o4.w = __funnelshift_r(v[3], v[4], sh);
+      *reinterpret_cast<uint4*>(out + x0) = o4;
+      return;
+    }
+  }
+  uint32_t words[4] = {0, 0, 0, 0};
+  int gxc = -1, dx = 0, sy = 0;
+  for (int e = 0; e < n; ++e) {
+    const int x = x0 + e;
+    const int gx = x / a.B;
+    if (gx != gxc) {
+      gxc = gx;
+      const int c = gy * a.gw + gx;
+      dx = __ldg(mv + 2 * c) * a.scale;
+      const int dy = __ldg(mv + 2 * c + 1) * a.scale;
+      sy = min(max(y + dy, 0), a.H - 1);
+    }
+    const int sx = min(max(x + dx, 0), a.W - 1);
+    words[e >> 2] |= (uint32_t)__ldcg(src + (long long)sy * a.W + sx) << (8 * (e & 3));
+  }
+  if (vec_ok && n == 16) {
+    *reinterpret_cast<uint4*>(out + x0) = make_uint4(words[0], words[1], words[2], words[3]);
+  } else {
+    for (int e = 0; e < n; ++e) out[x0 + e] = (uint8_t)(words[e >> 2] >> (8 * (e & 3)));
+  }
+}
+
+// The label chain of frames [t_begin, t_end) (pipeline.py:123-126).  Phase 1
+// copies every key frame's injected labels at once: the copies are
+// independent, so the whole grid streams them with four 16-byte loads in
+// flight per thread.  Phase 2 walks the non-key frames in order with a grid
+// barrier only where a frame reads one written earlier in this phase.
+constexpr int kChainKindsSmem = 2048;
 __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictArgs a, int n_streams, int t_begin,
                                                                  int t_end, unsigned* barrier_ctr) {
+  __shared__ int kind_s[kChainKindsSmem];
   const int groups_per_row = (a.W + 15) / 16;
   const long long per_stream = (long long)a.H * groups_per_row;
   const long long total = per_stream * n_streams;
+  const int nt = t_end - t_begin;
   const bool vec_ok = (a.W % 16 == 0) && (a.fs % 16 == 0) && (a.ss % 16 == 0) &&
                       ((reinterpret_cast<uintptr_t>(a.labels) & 15) == 0) &&
                       (!a.key_labels || (reinterpret_cast<uintptr_t>(a.key_labels) & 15) == 0);
-  unsigned epoch = 0;
-  for (int t = t_begin; t < t_end; ++t) {
-    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
-         g += (long long)gridDim.x * blockDim.x) {
-      const int stream = (int)(g / per_stream);
+  const bool ks = a.kind && (long long)n_streams * nt <= kChainKindsSmem;
+  if (ks)
+    for (int i = threadIdx.x; i < n_streams * nt; i += blockDim.x)
+      kind_s[i] = a.kind[(long long)(i / nt) * a.kss + t_begin + i % nt];
+  __syncthreads();
+  auto kind_of = [&](int stream, int t) -> int {
+    if (!a.kind) return 1;
+    return ks ? kind_s[stream * nt + (t - t_begin)] : a.kind[(long long)stream * a.kss + t];
+  };
+  auto frame_has = [&](int t, bool key) {
+    for (int st = 0; st < n_streams; ++st)
+      if ((kind_of(st, t) == 0) == key) return true;
+    return false;
+  };
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // ---- phase 1: key frames
+  bool any_nonkey = false;
+  if (a.kind) {
+    for (int t = t_begin; t < t_end; ++t) any_nonkey |= frame_has(t, false);
+    const long long lim = total * nt;
+    auto key_src = [&](long long idx, int& stream, int& t, long long& off) {
+      t = t_begin + (int)(idx / total);
+      const long long g = idx - (long long)(t - t_begin) * total;
+      stream = (int)(g / per_stream);
       const long long gg = g - stream * per_stream;
       const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
-      const long long o = (long long)stream * a.kss + t;
-      const int kind = a.kind ? a.kind[o] : 1;
-      uint8_t* out = a.labels + stream * a.ss + t * a.fs + (long long)y * a.W;
-      const int n = min(16, a.W - x0);
-      if (kind == 0) {
-        const uint8_t* src = a.key_labels + stream * a.ss + t * a.fs + (long long)y * a.W;
-        if (vec_ok) {
-          *reinterpret_cast<uint4*>(out + x0) = __ldcs(reinterpret_cast<const uint4*>(src + x0));
-        } else {
-          for (int e = 0; e < n; ++e) out[x0 + e] = src[x0 + e];
-        }
-        continue;
-      }
-      const int r = a.ref ? a.ref[o] : a.ref_fixed;
-      const uint8_t* src = a.labels + stream * a.ss + (long long)r * a.fs;
-      const int32_t* mv = a.mv + stream * a.mvss + t * a.mvfs;
-      if (a.matched) out = a.scratch + (long long)stream * a.H * a.W + (long long)y * a.W;  // refined below
-      const int gy = y / a.B;
-      const int gx0 = x0 / a.B, gx1 = (x0 + n - 1) / a.B;
-      if (vec_ok && n == 16 && gx0 == gx1) {
-        const int c = gy * a.gw + gx0;
-        const int dx = __ldg(mv + 2 * c) * a.scale, dy = __ldg(mv + 2 * c + 1) * a.scale;
-        const int sy = min(max(y + dy, 0), a.H - 1);
-        const int sx = x0 + dx;
-        if (sx >= 0 && sx + 16 <= a.W) {
-          const uint32_t* row = reinterpret_cast<const uint32_t*>(src + (long long)sy * a.W);
-          const int w0 = sx >> 2, sh = (sx & 3) * 8;
-          uint32_t v[5];
+      off = stream * a.ss + t * a.fs + (long long)y * a.W + x0;
+      return min(16, a.W - x0);
+    };
+    if (vec_ok) {
+      for (long long i0 = gtid; i0 < lim; i0 += 4 * stride) {
+        uint4 v[4];
+        long long off[4];
+        bool k[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] = __ldcg(row + w0 + q);
-          v[4] = sh ? __ldcg(row + w0 + 4) : 0u;
-          uint4 o4;
-          o4.x = __funnelshift_r(v[0], v[1], sh);
-          o4.y = __funnelshift_r(v[1], v[2], sh);
-          o4.z = __funnelshift_r(v[2], v[3], sh);
-          o4.w = __funnelshift_r(v[3], v[4], sh);
-          *reinterpret_cast<uint4*>(out + x0) = o4;
-          continue;
+        for (int u = 0; u < 4; ++u) {
+          const long long idx = i0 + u * stride;
+          k[u] = false;
+          if (idx < lim) {
+            int stream, t;
+            key_src(idx, stream, t, off[u]);
+            k[u] = kind_of(stream, t) == 0;
+            if (k[u]) v[u] = __ldcs(reinterpret_cast<const uint4*>(a.key_labels + off[u]));
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k[u]) *reinterpret_cast<uint4*>(a.labels + off[u]) = v[u];
       }
-      uint32_t words[4] = {0, 0, 0, 0};
-      int gxc = -1, dx = 0, sy = 0;
-      for (int e = 0; e < n; ++e) {
-        const int x = x0 + e;
-        const int gx = x / a.B;
-        if (gx != gxc) {
-          gxc = gx;
-          const int c = gy * a.gw + gx;
-          dx = __ldg(mv + 2 * c) * a.scale;
-          const int dy = __ldg(mv + 2 * c + 1) * a.scale;
-          sy = min(max(y + dy, 0), a.H - 1);
-        }
-        const int sx = min(max(x + dx, 0), a.W - 1);
-        words[e >> 2] |= (uint32_t)__ldcg(src + (long long)sy * a.W + sx) << (8 * (e & 3));
+    } else {
+      for (long long idx = gtid; idx < lim; idx += stride) {
+        int stream, t;
+        long long off;
+        const int n = key_src(idx, stream, t, off);
+        if (kind_of(stream, t) == 0)
+          for (int e = 0; e < n; ++e) a.labels[off + e] = a.key_labels[off + e];
       }
-      if (vec_ok && n == 16) {
-        *reinterpret_cast<uint4*>(out + x0) = make_uint4(words[0], words[1], words[2], words[3]);
-      } else {
-        for (int e = 0; e < n; ++e) out[x0 + e] = (uint8_t)(words[e >> 2] >> (8 * (e & 3)));
-      }
+    }
+    if (!any_nonkey) return;
+  }
+  unsigned epoch = 0;
+  if (a.kind) grid_barrier(barrier_ctr, ++epoch * gridDim.x);  // key frames visible to the gathers
+  // ---- phase 2: non-key frames in order
+  bool prev_wrote = false;
+  for (int t = t_begin; t < t_end; ++t) {
+    const bool work = !a.kind || frame_has(t, false);
+    if (!work) continue;
+    // frame t reads frames <= t-1, and its gather reuses the ring-vote scratch:
+    // any phase-2 work since the last barrier needs one first
+    if (prev_wrote) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
+    for (long long g = gtid; g < total; g += stride) {
+      const int stream = (int)(g / per_stream);
+      if (kind_of(stream, t) == 0) continue;
+      const long long gg = g - stream * per_stream;
+      const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
+      chain_gather_group(a, stream, t, (long long)stream * a.kss + t, y, x0, vec_ok);
     }
     if (a.matched) {
-      bool any_pred = !a.kind;
-      for (int st = 0; st < n_streams && !any_pred; ++st) any_pred = a.kind[(long long)st * a.kss + t] != 0;
-      if (any_pred) {
-        grid_barrier(barrier_ctr, ++epoch * gridDim.x);  // the whole unrefined prediction of frame t is written
-        ring_vote_frame(a, n_streams, t, total, per_stream, groups_per_row);
-      }
+      grid_barrier(barrier_ctr, ++epoch * gridDim.x);  // the whole unrefined prediction of frame t is written
+      ring_vote_frame(a, n_streams, t, total, per_stream, groups_per_row);
     }
-    if (t + 1 < t_end) {
-      // frame t+1 reads labels of frames <= t only when it is not a key frame (in any stream)
-      bool dep = !a.kind;
-      for (int st = 0; st < n_streams && !dep; ++st) dep = a.kind[(long long)st * a.kss + t + 1] != 0;
-      if (dep) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
-    }
+    prev_wrote = true;
   }
 }
 
