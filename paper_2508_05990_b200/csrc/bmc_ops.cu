@@ -646,7 +646,7 @@ __device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int str
 
 // The label chain of frames [t_begin, t_end) (pipeline.py:123-126).  Phase 1
 // copies every key frame's injected labels at once: the copies are
-// independent, so the whole grid streams them with four 16-byte loads in
+// independent, so the whole grid streams them with eight 16-byte loads in
 // flight per thread.  Phase 2 walks the non-key frames in order with a grid
 // barrier only where a frame reads one written earlier in this phase.
 constexpr int kChainKindsSmem = 2048;
@@ -680,43 +680,33 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
   bool any_nonkey = false;
   if (a.kind) {
     for (int t = t_begin; t < t_end; ++t) any_nonkey |= frame_has(t, false);
-    const long long lim = total * nt;
-    auto key_src = [&](long long idx, int& stream, int& t, long long& off) {
-      t = t_begin + (int)(idx / total);
-      const long long g = idx - (long long)(t - t_begin) * total;
-      stream = (int)(g / per_stream);
+    // one 16-pixel group per thread, its key frames eight at a time: the
+    // group's coordinates are computed once and eight loads are in flight
+    constexpr int U = 8;
+    for (long long g = gtid; g < total; g += stride) {
+      const int stream = (int)(g / per_stream);
       const long long gg = g - stream * per_stream;
       const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
-      off = stream * a.ss + t * a.fs + (long long)y * a.W + x0;
-      return min(16, a.W - x0);
-    };
-    if (vec_ok) {
-      for (long long i0 = gtid; i0 < lim; i0 += 4 * stride) {
-        uint4 v[4];
-        long long off[4];
-        bool k[4];
+      const long long base = stream * a.ss + (long long)y * a.W + x0;
+      const int n = min(16, a.W - x0);
+      for (int t0 = t_begin; t0 < t_end; t0 += U) {
+        if (vec_ok) {
+          uint4 v[U];
+          bool k[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const long long idx = i0 + u * stride;
-          k[u] = false;
-          if (idx < lim) {
-            int stream, t;
-            key_src(idx, stream, t, off[u]);
-            k[u] = kind_of(stream, t) == 0;
-            if (k[u]) v[u] = __ldcs(reinterpret_cast<const uint4*>(a.key_labels + off[u]));
+          for (int u = 0; u < U; ++u) {
+            const int t = t0 + u;
+            k[u] = t < t_end && kind_of(stream, t) == 0;
+            if (k[u]) v[u] = __ldcs(reinterpret_cast<const uint4*>(a.key_labels + base + t * a.fs));
           }
-        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (k[u]) *reinterpret_cast<uint4*>(a.labels + off[u]) = v[u];
-      }
-    } else {
-      for (long long idx = gtid; idx < lim; idx += stride) {
-        int stream, t;
-        long long off;
-        const int n = key_src(idx, stream, t, off);
-        if (kind_of(stream, t) == 0)
-          for (int e = 0; e < n; ++e) a.labels[off + e] = a.key_labels[off + e];
+          for (int u = 0; u < U; ++u)
+            if (k[u]) *reinterpret_cast<uint4*>(a.labels + base + (t0 + u) * a.fs) = v[u];
+        } else {
+          for (int t = t0; t < min(t0 + U, t_end); ++t)
+            if (kind_of(stream, t) == 0)
+              for (int e = 0; e < n; ++e) a.labels[base + t * a.fs + e] = a.key_labels[base + t * a.fs + e];
+        }
       }
     }
     if (!any_nonkey) return;
