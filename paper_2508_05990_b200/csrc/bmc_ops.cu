@@ -27,51 +27,77 @@ __device__ __forceinline__ uint32_t pack_pick(const Elem* __restrict__ row, int 
   return word;
 }
 
-// One thread turns 8 raw bytes of one raw row into one 32-bit word of each of
-// the two CFA planes that row feeds (even / odd columns, split with PRMT), so
-// reads and writes are both coalesced 8- / 4-byte accesses.  blockIdx.y walks
-// (frame, plane row, raw-row parity); words that touch the right padding take
-// the clamped per-sample path.
+// One thread turns one 16-byte chunk of a raw row into two 32-bit words of
+// each of the two CFA planes that row feeds (even / odd columns, split with
+// PRMT): 16-byte loads, 8-byte stores.  A CTA walks kPackRows consecutive
+// (frame, plane row, raw-row parity) rows; words that touch the right padding
+// (or rows whose layout is not 16-byte aligned) take the clamped per-sample path.
+constexpr int kPackRows = 8;
+template <typename Elem>
+__device__ __forceinline__ void pack_split(uint32_t a, uint32_t b, uint32_t& ev, uint32_t& od) {
+  if constexpr (sizeof(Elem) == 1) {
+    ev = __byte_perm(a, b, 0x6420);
+    od = __byte_perm(a, b, 0x7531);
+  } else {
+    ev = __byte_perm(a, b, 0x5410);
+    od = __byte_perm(a, b, 0x7632);
+  }
+}
+
 template <typename Elem>
 __global__ void pack_kernel(const Elem* __restrict__ raw, int kind, int H, int W, const bmc_fme_params p,
-                            Elem* __restrict__ planes) {
+                            Elem* __restrict__ planes, int n_rows) {
   constexpr int EPW = 4 / sizeof(Elem);
   const int wpr = p.pitch / EPW;
   const bool bayer = kind == BMC_KIND_BAYER;
-  const int par = bayer ? 2 : 1;
-  const int rowsel = blockIdx.y;  // (f * pad_h + y) * par + parity
-  const int parity = bayer ? (rowsel & 1) : 0;
-  const int fy = bayer ? (rowsel >> 1) : rowsel;
-  const int f = fy / p.pad_h, y = fy - f * p.pad_h;
-  const int ys = min(y, p.real_h - 1);
-  const Elem* frame = raw + (long long)f * H * W;
-  Elem* out = planes + (long long)f * p.frame_stride + (long long)y * p.pitch;
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < wpr; w += gridDim.x * blockDim.x) {
+  const bool vec = bayer && (W % (4 * EPW)) == 0 && (p.pitch % (2 * EPW)) == 0 && (p.plane_stride % (2 * EPW)) == 0 &&
+                   (p.frame_stride % (2 * EPW)) == 0;
+  for (int rr = 0; rr < kPackRows; ++rr) {
+    const int rowsel = blockIdx.x * kPackRows + rr;  // (f * pad_h + y) * par + parity
+    if (rowsel >= n_rows) return;
+    const int parity = bayer ? (rowsel & 1) : 0;
+    const int fy = bayer ? (rowsel >> 1) : rowsel;
+    const int f = fy / p.pad_h, y = fy - f * p.pad_h;
+    const int ys = min(y, p.real_h - 1);
+    const Elem* frame = raw + (long long)f * H * W;
+    Elem* out = planes + (long long)f * p.frame_stride + (long long)y * p.pitch;
     if (!bayer) {
       const Elem* row = frame + (long long)ys * W;
-      const uint32_t word = ((w + 1) * EPW <= p.real_w && (W % EPW) == 0)
-                                ? __ldg(reinterpret_cast<const uint32_t*>(row) + w)
-                                : pack_pick<Elem>(row, 0, 1, w, p.real_w);
-      reinterpret_cast<uint32_t*>(out)[w] = word;
+      for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
+        const uint32_t word = ((w + 1) * EPW <= p.real_w && (W % EPW) == 0)
+                                  ? __ldg(reinterpret_cast<const uint32_t*>(row) + w)
+                                  : pack_pick<Elem>(row, 0, 1, w, p.real_w);
+        reinterpret_cast<uint32_t*>(out)[w] = word;
+      }
       continue;
     }
     const Elem* row = frame + (long long)(2 * ys + parity) * W;
-    uint32_t ev, od;
-    if ((w + 1) * EPW <= p.real_w && (W % (2 * EPW)) == 0) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(row) + w);  // 2*EPW raw samples
-      if constexpr (EPW == 4) {
-        ev = __byte_perm(v.x, v.y, 0x6420);
-        od = __byte_perm(v.x, v.y, 0x7531);
-      } else {
-        ev = __byte_perm(v.x, v.y, 0x5410);
-        od = __byte_perm(v.x, v.y, 0x7632);
+    uint32_t* oe = reinterpret_cast<uint32_t*>(out + (2 * parity) * p.plane_stride);
+    uint32_t* oo = reinterpret_cast<uint32_t*>(out + (2 * parity + 1) * p.plane_stride);
+    for (int w2 = threadIdx.x; w2 < (wpr + 1) / 2; w2 += blockDim.x) {  // output word pair (2*w2, 2*w2+1)
+      const int w = 2 * w2;
+      if (vec && (w + 2) * EPW <= p.real_w && w + 1 < wpr) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + w2);  // 4*EPW raw samples
+        uint2 e2, o2;
+        pack_split<Elem>(v.x, v.y, e2.x, o2.x);
+        pack_split<Elem>(v.z, v.w, e2.y, o2.y);
+        reinterpret_cast<uint2*>(oe)[w2] = e2;
+        reinterpret_cast<uint2*>(oo)[w2] = o2;
+        continue;
       }
-    } else {
-      ev = pack_pick<Elem>(row, 0, 2, w, p.real_w);
-      od = pack_pick<Elem>(row, 1, 2, w, p.real_w);
+      for (int ww = w; ww < min(w + 2, wpr); ++ww) {
+        uint32_t ev, od;
+        if ((ww + 1) * EPW <= p.real_w && (W % (2 * EPW)) == 0) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(row) + ww);  // 2*EPW raw samples
+          pack_split<Elem>(v.x, v.y, ev, od);
+        } else {
+          ev = pack_pick<Elem>(row, 0, 2, ww, p.real_w);
+          od = pack_pick<Elem>(row, 1, 2, ww, p.real_w);
+        }
+        oe[ww] = ev;
+        oo[ww] = od;
+      }
     }
-    reinterpret_cast<uint32_t*>(out + (2 * parity) * p.plane_stride)[w] = ev;
-    reinterpret_cast<uint32_t*>(out + (2 * parity + 1) * p.plane_stride)[w] = od;
   }
 }
 
@@ -80,28 +106,23 @@ int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p
   const int wpr = p.pitch / epw;
   const int par = kind == BMC_KIND_BAYER ? 2 : 1;
   const int rows_per_frame = p.pad_h * par;
-  if (rows_per_frame > 65535) {
-    set_error("frame too tall for the pack kernel");
-    return BMC_E_ARG;
-  }
   const int H = p.planes == 4 ? p.real_h * 2 : p.real_h;
   const int W = p.planes == 4 ? p.real_w * 2 : p.real_w;
-  const int tpb = 128;
-  const unsigned gx = (unsigned)((wpr + tpb - 1) / tpb);
-  const int frames_per_launch = 65535 / rows_per_frame;  // grid.y limit
-  const size_t eb = p.elem_bytes;
-  for (int f0 = 0; f0 < n_frames; f0 += frames_per_launch) {
-    const int nf = n_frames - f0 < frames_per_launch ? n_frames - f0 : frames_per_launch;
-    const char* rawp = (const char*)raw + (long long)f0 * H * W * eb;
-    char* pl = (char*)planes + (long long)f0 * p.frame_stride * eb;
-    const dim3 grid(gx, (unsigned)(nf * rows_per_frame));
-    if (p.elem_bytes == 1)
-      pack_kernel<uint8_t><<<grid, tpb, 0, st>>>((const uint8_t*)rawp, kind, H, W, p, (uint8_t*)pl);
-    else
-      pack_kernel<uint16_t><<<grid, tpb, 0, st>>>((const uint16_t*)rawp, kind, H, W, p, (uint16_t*)pl);
-    const int rc = cuda_status(cudaGetLastError(), "pack_kernel");
-    if (rc) return rc;
+  const int need = kind == BMC_KIND_BAYER ? (wpr + 1) / 2 : wpr;  // threads per row
+  const int tpb = need <= 128 ? 128 : (need <= 256 ? 256 : 512);
+  const long long n_rows = (long long)n_frames * rows_per_frame;
+  if (n_rows > 0x7fffffffLL) {
+    set_error("clip too large for the pack kernel");
+    return BMC_E_ARG;
   }
+  const unsigned grid = (unsigned)((n_rows + kPackRows - 1) / kPackRows);
+  if (grid == 0) return BMC_OK;
+  if (p.elem_bytes == 1)
+    pack_kernel<uint8_t><<<grid, tpb, 0, st>>>((const uint8_t*)raw, kind, H, W, p, (uint8_t*)planes, (int)n_rows);
+  else
+    pack_kernel<uint16_t><<<grid, tpb, 0, st>>>((const uint16_t*)raw, kind, H, W, p, (uint16_t*)planes, (int)n_rows);
+  const int rc = cuda_status(cudaGetLastError(), "pack_kernel");
+  if (rc) return rc;
   return BMC_OK;
 }
 
