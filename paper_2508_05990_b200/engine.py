@@ -80,12 +80,20 @@ class ClipEngine:
         self.ch, self.cw = p.pad_h // coarse, p.pad_w // coarse
         self.sp = N.select_params(self.gh, self.gw, coarse // self.b_final, self.ch, self.cw, config.aem_statistic,
                                   config.reference_policy, config.max_gop, config.aem_threshold)
-        self.acc = torch.zeros((S, self.ch, self.cw), dtype=torch.float64, device=self.dev)
-        self.fsk = torch.zeros(S, dtype=torch.int32, device=self.dev)
-        self.last_key = torch.zeros(S, dtype=torch.int32, device=self.dev)
-        self.kind = torch.zeros((S, T), dtype=torch.int32, device=self.dev)
+        # AEM state zeroed at the start of every step: one byte buffer carved into
+        # typed views (8-byte aligned) so the reset is one fill + the ref fill
+        n_acc, n_tr = S * self.ch * self.cw, S * T
+        n_i32 = 2 * S + S * T
+        n_i32 += n_i32 % 2
+        self._aem_zero = torch.zeros(8 * (n_acc + n_tr) + 4 * n_i32, dtype=torch.uint8, device=self.dev)
+        z = self._aem_zero
+        self.acc = z[:8 * n_acc].view(torch.float64).view(S, self.ch, self.cw)
+        self.trigger = z[8 * n_acc:8 * (n_acc + n_tr)].view(torch.float64).view(S, T)
+        ints = z[8 * (n_acc + n_tr):].view(torch.int32)
+        self.fsk = ints[:S]
+        self.last_key = ints[S:2 * S]
+        self.kind = ints[2 * S:2 * S + S * T].view(S, T)
         self.ref = torch.full((S, T), -1, dtype=torch.int32, device=self.dev)
-        self.trigger = torch.zeros((S, T), dtype=torch.float64, device=self.dev)
         self.workspace = torch.zeros(4, dtype=torch.int32, device=self.dev)  # label-chain grid barrier
         self.set_label_size(*(label_hw or (self.H, self.W)))
         self.graph = None
@@ -120,12 +128,8 @@ class ClipEngine:
         return (N.LevelOut * len(out))(*out)
 
     def _reset_state(self) -> None:
-        self.acc.zero_()
-        self.fsk.zero_()
-        self.last_key.zero_()
-        self.kind.zero_()
+        self._aem_zero.zero_()  # acc, trigger, frames_since_key, last_key, kind
         self.ref.fill_(-1)
-        self.trigger.zero_()
         if self.cfg.reference_policy == "keyframe":
             self.ref_index.copy_(self.ref_index_init)
 
