@@ -65,7 +65,12 @@ typedef struct bmc_level_out {
 } bmc_level_out;
 
 /* Library / device setup. */
+#define BMC_ABI_VERSION 2
 const char* bmc_version(void);
+int bmc_abi_version(void);          /* == BMC_ABI_VERSION of the build                     */
+size_t bmc_struct_size(int which);  /* sizeof: 0 bmc_fme_params, 1 bmc_level_out, 2 bmc_select_params */
+/* Byte fill of device memory on `stream` (state resets inside captured steps). */
+int bmc_memset_async(void* dst, int value, size_t bytes, void* stream);
 const char* bmc_last_error(void);
 int bmc_fill_params(bmc_fme_params* p, int kind, int elem_bytes, int height, int width,
                     int n_levels, const int32_t* block_sizes, const int32_t* stage_range,

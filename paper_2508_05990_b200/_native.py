@@ -9,14 +9,11 @@ product path raises.
 from __future__ import annotations
 
 import ctypes
-import math
 import threading
 from pathlib import Path
 
-import os
-
-# BMC_LIB_PATH lets kernel-variant experiments (tools/) point at another build.
-_LIB_PATH = Path(os.environ.get("BMC_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libbmc_b200.so")
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libbmc_b200.so"
+ABI_VERSION = 2  # must equal BMC_ABI_VERSION (include/bmc.h)
 
 BMC_OK, BMC_E_ARG, BMC_E_CUDA, BMC_E_NOVALID, BMC_E_SMEM = 0, 1, 2, 3, 4
 KIND_LUMA, KIND_BAYER = 0, 1
@@ -53,6 +50,9 @@ class SelectParams(ctypes.Structure):
 
 _SIGNATURES = {
     "bmc_version": (ctypes.c_char_p, []),
+    "bmc_abi_version": (ctypes.c_int, []),
+    "bmc_struct_size": (ctypes.c_size_t, [ctypes.c_int]),
+    "bmc_memset_async": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_size_t, vp]),
     "bmc_last_error": (ctypes.c_char_p, []),
     "bmc_fill_params": (ctypes.c_int, [ctypes.POINTER(FmeParams), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, ctypes.c_int, ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -88,18 +88,21 @@ def lib_path() -> Path:
 
 
 def load(build_if_missing: bool = True):
-    """Load (and, in a source checkout, build) the shared library."""
+    """Load (and, in a source checkout, rebuild when stale) the shared library.
+
+    A rebuild that was needed and failed raises: loading the previous .so
+    would run kernels that no longer match the sources or the ctypes layouts.
+    The loaded library's ABI version and struct sizes are checked against this
+    module before any call is made.
+    """
     global _lib
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing and "BMC_LIB_PATH" not in os.environ:
+        if build_if_missing:
             from . import build as _build
-            try:
-                _build.build()
-            except Exception:
-                if not _LIB_PATH.exists():
-                    raise
+            if _build.sources_present():
+                _build.build()  # file-locked; raises on a compile error
         if not _LIB_PATH.exists():
             raise ImportError(f"libbmc_b200.so not found at {_LIB_PATH}; run paper_2508_05990_b200/build.py")
         lib = ctypes.CDLL(str(_LIB_PATH))
@@ -107,6 +110,13 @@ def load(build_if_missing: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        abi = lib.bmc_abi_version()
+        if abi != ABI_VERSION:
+            raise ImportError(f"{_LIB_PATH} has ABI {abi}, the Python binding expects {ABI_VERSION}; rebuild it")
+        for code, st in ((0, FmeParams), (1, LevelOut), (2, SelectParams)):
+            if lib.bmc_struct_size(code) != ctypes.sizeof(st):
+                raise ImportError(f"{_LIB_PATH}: {st.__name__} is {lib.bmc_struct_size(code)} bytes in C, "
+                                  f"{ctypes.sizeof(st)} in the binding; rebuild it")
         _lib = lib
         return lib
 
@@ -127,6 +137,12 @@ def require_cuda():
         raise RuntimeError("paper_2508_05990_b200 runs on CUDA (sm_100a) only; no CUDA device is visible "
                            "and there is no CPU fallback")
     return torch
+
+
+def memset_async(tensor, value: int, stream=None) -> None:
+    """Byte fill of a device tensor on the current stream (a memset node under graph capture)."""
+    check(load().bmc_memset_async(ptr(tensor), int(value), tensor.numel() * tensor.element_size(),
+                                  stream_handle(stream)))
 
 
 def stream_handle(stream=None) -> int:

@@ -3,10 +3,14 @@ travels with the repo snapshot to the GPU box).
 
 Each .cu is compiled to an object in parallel (the stage-kernel
 instantiation units dominate the build), then linked into one shared library.
+Builds are serialised across processes with an fcntl lock (torchrun ranks that
+all find a stale library build it once), objects and the library are written
+under per-process temporary names and renamed into place.
 """
 
 from __future__ import annotations
 
+import fcntl
 import os
 import subprocess
 import sys
@@ -17,11 +21,17 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "lib" / "libbmc_b200.so"
-SOURCES = ["bmc_api.cu", "bmc_fme.cu", "bmc_fme_k_u8c4.cu", "bmc_fme_k_u8c2.cu", "bmc_fme_k_u16.cu", "bmc_fme_small.cu",
-           "bmc_ops.cu"]
-HEADERS = ["bmc_internal.cuh", "bmc_launch.cuh", "bmc_fme_impl.cuh"]
+LOCK = PKG / "lib" / ".build.lock"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+
+
+def sources():
+    return sorted(p.name for p in CSRC.glob("*.cu"))
+
+
+def sources_present() -> bool:
+    return CSRC.is_dir() and any(CSRC.glob("*.cu"))
 
 
 def nvcc() -> str:
@@ -30,7 +40,8 @@ def nvcc() -> str:
 
 
 def _deps():
-    return [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "bmc.h", Path(__file__)]
+    return ([CSRC / s for s in sources()] + sorted(CSRC.glob("*.cuh")) + sorted((ROOT / "include").glob("*.h"))
+            + [Path(__file__)])
 
 
 def _stale() -> bool:
@@ -40,34 +51,49 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in _deps())
 
 
-def _compile(src: str, obj: Path, verbose: bool):
-    cmd = [nvcc(), *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-I", str(ROOT / "include"),
-           "-c", str(CSRC / src), "-o", str(obj)]
-    return subprocess.run(cmd, capture_output=True, text=True)
+def _compile(src: str, obj: Path, verbose: bool, extra=()):
+    tmp = obj.with_name(f"{obj.name}.{os.getpid()}.tmp")
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-Xptxas", "-v" if verbose else "-O3", "-I", str(ROOT / "include"),
+           "-c", str(CSRC / src), "-o", str(tmp)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode == 0:
+        os.replace(tmp, obj)
+    return res
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    objdir = PKG / "lib" / "obj"
-    objdir.mkdir(parents=True, exist_ok=True)
-    objs = [objdir / (Path(s).stem + ".o") for s in SOURCES]
-    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
-        results = list(ex.map(lambda so: _compile(so[0], so[1], verbose), zip(SOURCES, objs)))
-    for src, res in zip(SOURCES, results):
-        if res.returncode != 0:
-            sys.stderr.write(res.stdout + res.stderr)
-            raise RuntimeError(f"nvcc failed compiling {src}")
-        if verbose:
-            sys.stderr.write(res.stderr)
-    tmp = LIB.with_suffix(".so.tmp")
-    res = subprocess.run([nvcc(), *ARCH, "--shared", "-o", str(tmp), *map(str, objs)],
-                         capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed linking libbmc_b200.so")
-    os.replace(tmp, LIB)
-    return LIB
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, extra=()) -> Path:
+    """Compile every csrc/*.cu and link the library.  ``extra`` nvcc flags and
+    ``out`` are for measurement builds (tools/), which go to their own path."""
+    target = Path(out) if out else LIB
+    target.parent.mkdir(parents=True, exist_ok=True)
+    LOCK.parent.mkdir(parents=True, exist_ok=True)
+    with open(LOCK, "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and out is None and not _stale():
+                return LIB
+            objdir = target.parent / ("obj" if out is None else f"obj_{target.stem}")
+            objdir.mkdir(parents=True, exist_ok=True)
+            srcs = sources()
+            objs = [objdir / (Path(s).stem + ".o") for s in srcs]
+            with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+                results = list(ex.map(lambda so: _compile(so[0], so[1], verbose, extra), zip(srcs, objs)))
+            for src, res in zip(srcs, results):
+                if res.returncode != 0:
+                    sys.stderr.write(res.stdout + res.stderr)
+                    raise RuntimeError(f"nvcc failed compiling {src}")
+                if verbose:
+                    sys.stderr.write(res.stderr)
+            tmp = target.with_name(f"{target.name}.{os.getpid()}.tmp")
+            res = subprocess.run([nvcc(), *ARCH, "--shared", "-o", str(tmp), *map(str, objs)],
+                                 capture_output=True, text=True)
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError("nvcc failed linking libbmc_b200.so")
+            os.replace(tmp, target)
+            return target
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
 
 
 if __name__ == "__main__":

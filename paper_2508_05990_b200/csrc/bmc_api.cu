@@ -67,6 +67,26 @@ const char* bmc_version(void) { return "bmc_b200 0.1.0 (sm_100a)"; }
 
 const char* bmc_last_error(void) { return g_err; }
 
+int bmc_abi_version(void) { return BMC_ABI_VERSION; }
+
+size_t bmc_struct_size(int which) {
+  switch (which) {
+    case 0: return sizeof(bmc_fme_params);
+    case 1: return sizeof(bmc_level_out);
+    case 2: return sizeof(bmc_select_params);
+    default: return 0;
+  }
+}
+
+int bmc_memset_async(void* dst, int value, size_t bytes, void* stream) {
+  if (!bytes) return BMC_OK;
+  if (!dst) {
+    set_error("NULL argument");
+    return BMC_E_ARG;
+  }
+  return cuda_status(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream), "bmc_memset_async");
+}
+
 int bmc_fill_params(bmc_fme_params* p, int kind, int elem_bytes, int height, int width, int n_levels,
                     const int32_t* block_sizes, const int32_t* stage_range, const int32_t* stage_step, double lam,
                     double sparsity_tolerance, double split_threshold, double refine_block_threshold) {
@@ -162,7 +182,7 @@ int bmc_pack_planes(const void* raw, int n_frames, int kind, const bmc_fme_param
 
 static int stage_kblk() {
   static const int v = [] {
-    const char* e = getenv("BMC_KBLK");
+    const char* e = knob_env("BMC_KBLK");
     const int k = e ? atoi(e) : 2;
     return k >= 1 && k <= 8 ? k : 2;
   }();
@@ -234,17 +254,11 @@ int bmc_estimate_motion(const void* planes, int n_frames, const bmc_fme_params* 
       std::memset(&a, 0, sizeof a);
       // level 0's first searched stage is centred on (0, 0) for every block: kblk horizontally
       // adjacent blocks share one staged window (fme.py:350-368 with mv = 0 at level 0)
-      if (plan_stage_ws(a.plan, *p, b, p->stage_range[s], p->stage_step[s])) {
-        // warp-specialized persistent kernel: screening overlaps staging and selection
+      a.kblk = (L == 0 && k == 0) ? stage_kblk() : 1;
+      rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, a.kblk);
+      if (rc == BMC_OK && a.kblk > 1 && !a.plan.use_tma) {
         a.kblk = 1;
-        rc = BMC_OK;
-      } else {
-        a.kblk = (L == 0 && k == 0) ? stage_kblk() : 1;
-        rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, a.kblk);
-        if (rc == BMC_OK && a.kblk > 1 && !a.plan.use_tma) {
-          a.kblk = 1;
-          rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, 1);
-        }
+        rc = plan_stage(a.plan, *p, b, p->stage_range[s], p->stage_step[s], true, 1);
       }
       if (rc) return rc;
       a.planes = planes;

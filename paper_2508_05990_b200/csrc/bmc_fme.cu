@@ -51,7 +51,7 @@ static int encode_map(CUtensorMap* m, const void* base, const bmc_fme_params& p,
 // at <= 72 registers so two 13-warp CTAs share an SM).
 static int pick_ty(int G) {
   static const int cap = [] {
-    const char* e = getenv("BMC_TY_MAX");
+    const char* e = knob_env("BMC_TY_MAX");
     const int v = e ? atoi(e) : 11;
     return v >= 1 && v <= 12 ? v : 11;
   }();
@@ -70,7 +70,7 @@ static const int kSmemTarget = 110 * 1024;
 // memory without the per-part partial-sum arrays.
 static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed, int kblk) {
   static const int max_threads = [] {
-    const char* e = getenv("BMC_MAX_THREADS");
+    const char* e = knob_env("BMC_MAX_THREADS");
     const int v = e ? atoi(e) : kMaxStageThreads;
     return v >= 64 && v <= kMaxStageThreads ? v / 32 * 32 : kMaxStageThreads / 32 * 32;
   }();
@@ -80,7 +80,7 @@ static void pick_parts(StagePlan& pl, int cols, int units_max, int smem_fixed, i
     const int smem = smem_fixed + ((kblk * parts * pl.nmax * 4 + 127) & ~127);
     const int by_smem = (228 * 1024) / (smem + 1024);
     static const int soft_cap = [] {
-      const char* e = getenv("BMC_CTA_CAP");
+      const char* e = knob_env("BMC_CTA_CAP");
       const int v = e ? atoi(e) : 256;
       return v >= 64 && v <= kMaxStageThreads ? v / 32 * 32 : 256;
     }();
@@ -151,11 +151,11 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
   const int wwin = 2 * r * s + b * kblk;  // kblk adjacent blocks share the window
   const int align = 16 / eb;  // TMA: inner box extent and start coordinate on 16-byte boundaries
   static const bool no_tma = [] {
-    const char* e = getenv("BMC_NO_TMA");
+    const char* e = knob_env("BMC_NO_TMA");
     return e && *e && *e != '0';
   }();
   static const bool no_copies = [] {  // pre-shifted copies measured slower than in-loop shifts
-    const char* e = getenv("BMC_COPIES");
+    const char* e = knob_env("BMC_COPIES");
     return !(e && *e && *e != '0');
   }();
   // TMA box: the window widened by up to align-1 leading elements (16-byte aligned start) + 1 word of slack
@@ -194,7 +194,7 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
       const int copy_words = (win_bytes / 4 + 31) / 32 * 32 + 8;  // bank skew of 8 words per phase
       const int total = off_win + (want_copies ? (ncopies - 1) * copy_words * 4 + win_bytes : win_bytes);
       static const bool full_planes_big = [] {  // allow all planes staged up to the full budget (1 CTA/SM)
-        const char* e = getenv("BMC_SMEM_SPLIT");
+        const char* e = knob_env("BMC_SMEM_SPLIT");
         return !(e && *e && *e != '0');
       }();
       if (total <= kSmemTarget || ((pg == 1 || (pg == p.planes && full_planes_big)) && total <= kSmemBudget)) {
@@ -223,7 +223,7 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     if (alt.pg > pl.pg) pl = alt;
   }
   static const bool no_pitch = [] {
-    const char* e = getenv("BMC_NO_PITCH");
+    const char* e = knob_env("BMC_NO_PITCH");
     return e && *e && *e != '0';
   }();
   if (pl.pg && pl.use_tma && !pl.copies && !no_pitch) {
@@ -269,13 +269,13 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     pl.per = pl.pg == p.planes ? (p.planes * cpr * nrho + pl.parts - 1) / pl.parts : 0;
     pl.mper = magic(pl.per > 0 ? pl.per : 1);
     static const bool no_split = [] {
-      const char* e = getenv("BMC_NO_SPLIT");
+      const char* e = knob_env("BMC_NO_SPLIT");
       return e && *e && *e != '0';
     }();
     pl.split = (!no_split && pl.per > 1) ? 1 : 0;
   }
   static const int debug_skip = [] {
-    const char* e = getenv("BMC_DEBUG_SKIP");
+    const char* e = knob_env("BMC_DEBUG_SKIP");
     return e ? atoi(e) : 0;
   }();
   pl.debug = debug_skip;
@@ -285,57 +285,6 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     return BMC_E_SMEM;
   }
   return BMC_OK;
-}
-
-// Plan of the warp-specialized persistent kernel (bmc_fme_ws.cuh): uint8
-// blocks with 4-word chunks, every plane staged in one TMA pass, <= 7
-// screening warps.  Layout: head (+ slot barriers / info), klist, then two slots
-// of {partial sums, current block, window}.
-bool plan_stage_ws(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s) {
-  static const bool off = [] {  // opt-in (BMC_WS=1): measured slower than the classic kernel on C2 (2.99 vs 1.85 ms)
-    const char* e = getenv("BMC_WS");
-    return !(e && *e == '1');
-  }();
-  if (off || p.elem_bytes != 1 || b / 4 < 4) return false;
-  StagePlan q;
-  if (plan_stage(q, p, b, r, s, true, 1) != BMC_OK) return false;
-  if (!q.use_tma || q.pg != p.planes || q.copies || q.threads > 224) return false;  // kWsScreenMax (bmc_fme_ws.cuh)
-  // persistent pipelines only pay off with many blocks per CTA
-  if ((long long)(p.pad_w / b) * (p.pad_h / b) < 4 * 148) return false;
-  const int head = (smem_head_bytes() + 8 * 8 + 2 * 32 + 127) & ~127;  // + slot barriers and infos
-  q.off_klist = head;
-  q.off_sad = q.off_klist + ((2 * q.nmax * 4 + 127) & ~127);
-  q.off_cur = q.off_sad + ((q.parts * q.nmax * 4 + 127) & ~127);
-  q.off_win = q.off_cur + ((q.cur_bytes + 127) & ~127);
-  q.slot_bytes = q.off_win + ((q.win_bytes + 127) & ~127) - q.off_sad;
-  q.smem = q.off_sad + 2 * q.slot_bytes;
-  if (q.smem > kSmemBudget) return false;
-  q.ws = 1;
-  pl = q;
-  return true;
-}
-
-// Dynamic work counters of the WS kernel: a ring of zeroed device words, one
-// per launch (allocated once, outside graph capture).
-unsigned* ws_work_counter(cudaStream_t st) {
-  static std::mutex mu;
-  static unsigned* ring[16] = {};
-  static unsigned next[16] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 16) return nullptr;
-  std::lock_guard<std::mutex> g(mu);
-  if (!ring[dev]) {
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return nullptr;
-    if (cudaMalloc(&ring[dev], 256 * sizeof(unsigned)) != cudaSuccess) {
-      ring[dev] = nullptr;
-      return nullptr;
-    }
-  }
-  unsigned* c = ring[dev] + (next[dev]++ % 256);
-  if (cudaMemsetAsync(c, 0, sizeof(unsigned), st) != cudaSuccess) return nullptr;
-  return c;
 }
 
 // Launch one stage.  The TMA maps view a.ref_planes (n_ref_frames frames) for

@@ -583,7 +583,7 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
     for (int i = 0; i < min(g.G, EPW); ++i) phase_mask |= 1u << ((g.d + i * s) % EPW);
 
   __syncthreads();  // previous users of smem are done; mbarrier init visible
-  if (pl.use_tma && pl.pg == pc.P && !(phase_mask & ~1u) && !(pl.debug & 2)) {
+  if (pl.use_tma && pl.pg == pc.P && !(phase_mask & ~1u) && !pl.debug) {
     // common case, one TMA pass: clear the atomic-accumulated sums while the
     // boxes are in flight; each thread's mbarrier wait then makes the staged
     // tiles visible to it, so no CTA barrier is needed after the wait
@@ -623,11 +623,13 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
       build_phase_copies<Elem>(L, pl, npl, phase_mask);
     }
     __syncthreads();
-    if (!(pl.debug & 2)) {
-      sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0, nblk);
-    } else {  // measurement only (BMC_DEBUG_SKIP=2): no screening, every SAD reads 0
+#ifdef BMC_EXPERIMENTS
+    if (pl.debug & 2) {  // measurement only (BMC_DEBUG_SKIP=2): no screening, every SAD reads 0
       for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
+      continue;
     }
+#endif
+    sad_items<Elem, CW, TY, SHIFT>(L, g, b, npl, pl, coff_w, p0 > 0, nblk);
   }
   __syncthreads();
   return g;
@@ -646,6 +648,7 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
   const int nt = blockDim.x, nw = nt >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = pc.P * b * b;
+#ifdef BMC_EXPERIMENTS
   if (pl.debug & 1) {  // measurement only (BMC_DEBUG_SKIP=1): no selection, report the centre
     StageResult res;
     res.dx = cx;
@@ -654,6 +657,7 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     res.nvalid = 1;
     return res;
   }
+#endif
   // valid candidates form a rectangle i in [ilo, ihi] x j in [jlo, jhi] (fme.py:250-253)
   const FastDiv fsd(s, pl.ms);
   auto fdiv = [&](int a) { return a >= 0 ? (int)fsd.div(a) : -(int)fsd.div(-a + s - 1); };  // floor(a / s)
@@ -1018,7 +1022,7 @@ inline int set_smem(K kern, int bytes) {
 inline bool sync_debug() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("BMC_SYNC_DEBUG");
+    const char* e = knob_env("BMC_SYNC_DEBUG");
     v = (e && *e && *e != '0') ? 1 : 0;
   }
   return v == 1;
@@ -1032,7 +1036,7 @@ inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageL
   la.gwg = (uint32_t)((a.gw + a.kblk - 1) / a.kblk);
   la.total = a.single ? 1u : la.gwg * (uint32_t)a.gh * (uint32_t)a.n_pairs;
   static const bool plan_log = [] {
-    const char* e = getenv("BMC_PLAN_LOG");
+    const char* e = knob_env("BMC_PLAN_LOG");
     return e && *e && *e != '0';
   }();
   if (plan_log)
@@ -1074,7 +1078,7 @@ inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageL
   }
   const long long work = (long long)grid.x * grid.y;
   static const int persist_mult = [] {  // resident waves per launch; 0 = one CTA per block
-    const char* e = getenv("BMC_PERSIST");
+    const char* e = knob_env("BMC_PERSIST");
     return e ? atoi(e) : 0;
   }();
   const long long capacity = persist_mult > 0 ? (long long)per_sm * sms * persist_mult : work;

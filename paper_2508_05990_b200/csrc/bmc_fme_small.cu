@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) fme_small_kernel(const Stage
 
 bool small_level_ok(const bmc_fme_params& p, int b) {
   static const bool off = [] {
-    const char* e = getenv("BMC_NO_SMALL");
+    const char* e = knob_env("BMC_NO_SMALL");
     return e && *e && *e != '0';
   }();
   if (off) return false;

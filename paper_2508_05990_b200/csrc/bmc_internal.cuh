@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/bmc.h"
@@ -17,6 +18,20 @@ namespace bmc {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+
+// ---------------------------------------------------------------------------
+// measurement knobs: environment switches read ONLY by experiment builds
+// (tools/build_variants.sh compiles with -DBMC_EXPERIMENTS); the product
+// library ignores the environment, so no variable can change its results.
+// ---------------------------------------------------------------------------
+inline const char* knob_env(const char* name) {
+#ifdef BMC_EXPERIMENTS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // ---------------------------------------------------------------------------
 // error plumbing

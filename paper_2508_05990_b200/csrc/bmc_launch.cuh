@@ -26,8 +26,6 @@ struct StagePlan {
   int off_sad, off_klist, off_cur, off_win;
   int smem;
   int debug;      // measurement switches (BMC_DEBUG_SKIP): 1 skip selection, 2 skip screening
-  int ws;         // 1: warp-specialized persistent kernel (bmc_fme_ws.cuh), double-buffered slots
-  int slot_bytes; // WS: distance between the two slots (sad + cur + win)
   // host-precomputed fast-division magics (fastdiv_magic) of the CTA-uniform divisors
   unsigned long long mG, mncg, mrho, mcpr, ms, mparts, mgw, mcells, mper;
   int split;      // split the partial last warp's items into one-unit sub-items (single-pass plans)
@@ -114,8 +112,6 @@ struct PredictArgs {
 };
 
 int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool allow_tma, int kblk = 1);
-bool plan_stage_ws(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s);
-unsigned* ws_work_counter(cudaStream_t st);
 int launch_fme_stage(const StageLaunch& a, int n_cur_frames, int n_ref_frames, dim3 grid, cudaStream_t st);
 bool small_level_ok(const bmc_fme_params& p, int b);
 int launch_fme_small(const StageLaunch& a, cudaStream_t st);

@@ -128,8 +128,8 @@ class ClipEngine:
         return (N.LevelOut * len(out))(*out)
 
     def _reset_state(self) -> None:
-        self._aem_zero.zero_()  # acc, trigger, frames_since_key, last_key, kind
-        self.ref.fill_(-1)
+        N.memset_async(self._aem_zero, 0)  # acc, trigger, frames_since_key, last_key, kind
+        N.memset_async(self.ref, 0xFF)  # int32 -1
         if self.cfg.reference_policy == "keyframe":
             self.ref_index.copy_(self.ref_index_init)
 

@@ -65,6 +65,58 @@ def bayer_pan_clip(width: int, height: int, frames: int, velocity, seed: int = 0
     return out
 
 
+# full-res velocity sweep (px/frame); odd steps are added on alternate segments
+C5_SWEEP = (0, 2, 8, 16, 24, 40, 64, 96, 200)
+
+
+def bayer_path_clip(width: int, height: int, path, seed: int = 0, pattern: FrameKind = FrameKind.BAYER_RGGB,
+                    dtype=np.uint8, square: int = 0, square_velocity=(0, 0)) -> np.ndarray:
+    """Like ``bayer_pan_clip`` but the crop origin follows ``path`` (one (x, y) full-res
+    offset per frame, any integers), so the pan velocity can change from frame to frame."""
+    path = [(int(x), int(y)) for x, y in path]
+    xs, ys = [p[0] for p in path], [p[1] for p in path]
+    mx, my = -min(xs) + 8, -min(ys) + 8
+    wc, hc = width + mx + max(xs) + 8, height + my + max(ys) + 8
+    chans = [value_noise(wc, hc, seed + k) for k in range(3)]
+    if square:
+        patch = [(value_noise(square, square, seed + 10 + k, cell=8) // 2 + 112).astype(np.uint8) for k in range(3)]
+        sx0, sy0 = width // 4, height // 4
+    out = np.empty((len(path), height, width), dtype=np.uint16 if np.dtype(dtype) == np.uint16 else np.uint8)
+    for t, (px, py) in enumerate(path):
+        x, y = mx + px, my + py
+        rgb = [c[y:y + height, x:x + width].copy() for c in chans]
+        if square:
+            qx = min(max(sx0 + square_velocity[0] * t, 0), width - square)
+            qy = min(max(sy0 + square_velocity[1] * t, 0), height - square)
+            for c, p in zip(rgb, patch):
+                c[qy:qy + square, qx:qx + square] = p
+        data = mosaic_rgb(*rgb, pattern=pattern).data
+        out[t] = data.astype(np.uint16) * 257 if out.dtype == np.uint16 else data
+    return out
+
+
+def c5_clip(width: int = 1920, height: int = 1080, frames: int = 40, seed: int = 7, cut_at: int = 30,
+            dtype=np.uint8) -> np.ndarray:
+    """high-motion Bayer sweep with a moving textured square and a scene cut.
+
+    Frames before ``cut_at`` pan with a piecewise-constant velocity stepping through
+    ``C5_SWEEP`` (three frames per step; odd steps +1 on alternate segments, vertical
+    component -vx/3), with a 192-px square moving at (13, -7); from ``cut_at`` on an
+    unrelated scene pans at (24, -16)."""
+    path, x, y = [], 0, 0
+    for t in range(cut_at):
+        if t:
+            k = min((t - 1) // 3, len(C5_SWEEP) - 1)
+            vx = C5_SWEEP[k] + (k % 2)
+            x, y = x + vx, y - vx // 3
+        path.append((x, y))
+    a = bayer_path_clip(width, height, path, seed=seed, dtype=dtype, square=192, square_velocity=(13, -7))
+    if frames <= cut_at:
+        return a[:frames]
+    b = bayer_pan_clip(width, height, frames - cut_at, (24, -16), seed=seed + 1000, dtype=dtype)
+    return np.concatenate([a, b])
+
+
 def scene_cut_clip(width: int, height: int, frames: int, cut_at: int, seed: int = 0, dtype=np.uint8) -> np.ndarray:
     """Static textured Bayer scene A before ``cut_at``, unrelated scene B after."""
     a = bayer_pan_clip(width, height, 1, (0, 0), seed, dtype=dtype)[0]

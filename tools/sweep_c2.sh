@@ -5,6 +5,6 @@ cfgs=${1:-c2}; caps=${2:-"416 256 224 160 128"}
 for c in $cfgs; do for mt in $caps; do
   BMC_MAX_THREADS=$mt VARIANT="default_mt$mt" timeout 200 python tools/time_me.py $c 8 2>&1 | tail -1
   for d in tools/variants/*/; do n=$(basename $d)
-    BMC_LIB_PATH=$PWD/$d/libbmc_b200.so BMC_MAX_THREADS=$mt VARIANT="${n}_mt$mt" timeout 200 python tools/time_me.py $c 8 2>&1 | tail -1
+    VARIANT_LIB=$PWD/$d/libbmc_b200.so BMC_MAX_THREADS=$mt VARIANT="${n}_mt$mt" timeout 200 python tools/time_me.py $c 8 2>&1 | tail -1
   done
 done; done

@@ -1,8 +1,10 @@
 """Time the ME launch of a config (CUDA events, L2 flushed between reps); prints one JSON line."""
 import sys, ctypes, json, os, statistics
-sys.path.insert(0, '.')
+sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
 import torch
 import bench
+import _variant
+_variant.use_variant_from_env()
 from paper_2508_05990_b200 import _native as N
 from paper_2508_05990_b200.engine import ClipEngine
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
