@@ -1,0 +1,59 @@
+/*
+ * bmc_ext.h — C ABI of the B200 back end's ingest, reporting and CaBR entry
+ * points (the callers and data formats either side of the hot
+ * path).  Same conventions as bmc.h: caller-allocated DEVICE buffers, plain
+ * pointers and sizes, an explicit CUDA stream passed as void*, int status
+ * (BMC_OK / BMC_E_ARG / BMC_E_CUDA), error text via bmc_last_error().
+ */
+#ifndef BMC_B200_EXT_H
+#define BMC_B200_EXT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- ingest --
+ * Raw sensor payloads -> uint16 frames, on device (frame_io.py:202-241 reads
+ * PGM on the host with numpy; here the payload is copied from pinned host
+ * memory as-is and decoded by the GPU).  Formats:
+ *   BMC_RAW_BE16  2 bytes/px big-endian (binary PGM with maxval >= 256,
+ *                 frame_io.py:230-235: np.dtype(">u2") then astype(uint16))
+ *   BMC_RAW_MIPI10 MIPI CSI-2 RAW10: 4 px in 5 bytes (4 MSB bytes, then one
+ *                 byte of 2-bit LSBs, pixel 0 in bits 1:0)
+ *   BMC_RAW_MIPI12 MIPI CSI-2 RAW12: 2 px in 3 bytes (2 MSB bytes, then one
+ *                 byte of 4-bit LSBs, pixel 0 in bits 3:0)
+ * src: n_frames payloads, frame f at src + f*src_frame_bytes, row y at
+ * + y*src_row_bytes.  dst: (n_frames, height, width) uint16, row-major.
+ * Each decoded value is shifted left by `shift` (0 keeps sensor codes,
+ * 16-bits left-aligns them to the uint16 range). */
+#define BMC_RAW_BE16 0
+#define BMC_RAW_MIPI10 1
+#define BMC_RAW_MIPI12 2
+int bmc_unpack_raw(const uint8_t* src, int64_t src_frame_bytes, int64_t src_row_bytes, int n_frames,
+                   int height, int width, int format, int shift, uint16_t* dst, void* stream);
+
+/* Inverse of the above for BMC_RAW_BE16 (frame_io.py:238-242 _write_pgm
+ * payload): uint16 frames -> big-endian bytes. */
+int bmc_pack_be16(const uint16_t* src, int64_t n, uint8_t* dst, void* stream);
+
+/* --------------------------------------------------------------- metrics --
+ * Confusion matrices of n_maps label-map pairs (metrics.py:70-98, the
+ * np.bincount(truth*num_classes + pred) of miou).  pred/truth: n_maps maps of
+ * n pixels, map i at + i*map_stride.  Pixels whose truth equals ignore_class
+ * are dropped (ignore_class < 0: none).  confusion: (n_maps, num_classes,
+ * num_classes) uint64, overwritten.  overflow (one device int32, may be NULL)
+ * is set to 1 when some truth*num_classes+pred >= num_classes^2 (numpy's
+ * bincount would then grow past the square and the reshape raises); those
+ * pixels are not counted.  num_classes <= 1024.  The float IoU/mean over the (tiny) matrix is done
+ * by the host in numpy's order. */
+int bmc_confusion(const uint8_t* pred, const uint8_t* truth, int64_t n, int n_maps, int64_t map_stride,
+                  int num_classes, int ignore_class, unsigned long long* confusion, int32_t* overflow,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMC_B200_EXT_H */

@@ -75,7 +75,14 @@ _SIGNATURES = {
                                                ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
     "bmc_predict_features": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]),
+    # include/bmc_ext.h: ingest, reporting
+    "bmc_unpack_raw": (ctypes.c_int, [vp, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, vp, vp]),
+    "bmc_pack_be16": (ctypes.c_int, [vp, i64, vp, vp]),
+    "bmc_confusion": (ctypes.c_int, [vp, vp, i64, ctypes.c_int, i64, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
 }
+
+RAW_BE16, RAW_MIPI10, RAW_MIPI12 = 0, 1, 2
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

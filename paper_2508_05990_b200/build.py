@@ -2,7 +2,8 @@
 travels with the repo snapshot to the GPU box).
 
 Each .cu is compiled to an object in parallel (the stage-kernel
-instantiation units dominate the build), then linked into one shared library.
+instantiation units dominate the build), then linked into one shared library;
+an object is recompiled only when its source or a header it includes changed.
 Builds are serialised across processes with an fcntl lock (torchrun ranks that
 all find a stale library build it once), objects and the library are written
 under per-process temporary names and renamed into place.
@@ -12,6 +13,7 @@ from __future__ import annotations
 
 import fcntl
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -42,6 +44,30 @@ def nvcc() -> str:
 def _deps():
     return ([CSRC / s for s in sources()] + sorted(CSRC.glob("*.cuh")) + sorted((ROOT / "include").glob("*.h"))
             + [Path(__file__)])
+
+
+_INC = re.compile(r'^\s*#\s*include\s+"([^"]+)"', re.M)
+
+
+def _includes(path: Path, seen=None) -> set:
+    """Local (quoted) headers a source pulls in, transitively."""
+    seen = set() if seen is None else seen
+    for name in _INC.findall(path.read_text()):
+        for cand in (path.parent / name, ROOT / "include" / name):
+            cand = cand.resolve()
+            if cand.exists() and cand not in seen:
+                seen.add(cand)
+                _includes(cand, seen)
+                break
+    return seen
+
+
+def _obj_stale(src: str, obj: Path) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    deps = [CSRC / src, Path(__file__), *_includes(CSRC / src)]
+    return any(d.stat().st_mtime > t for d in deps)
 
 
 def _stale() -> bool:
@@ -76,9 +102,12 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, e
             objdir.mkdir(parents=True, exist_ok=True)
             srcs = sources()
             objs = [objdir / (Path(s).stem + ".o") for s in srcs]
-            with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
-                results = list(ex.map(lambda so: _compile(so[0], so[1], verbose, extra), zip(srcs, objs)))
-            for src, res in zip(srcs, results):
+            # per-object staleness (source + transitively included headers); a forced
+            # or measurement build recompiles everything
+            todo = [(s, o) for s, o in zip(srcs, objs) if force or out is not None or _obj_stale(s, o)]
+            with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+                results = list(ex.map(lambda so: _compile(so[0], so[1], verbose, extra), todo))
+            for (src, _), res in zip(todo, results):
                 if res.returncode != 0:
                     sys.stderr.write(res.stdout + res.stderr)
                     raise RuntimeError(f"nvcc failed compiling {src}")

@@ -1,4 +1,4 @@
-"""CPU: the C-ABI library builds/loads, exports every symbol include/bmc.h
+"""CPU: the C-ABI library builds/loads, exports every symbol include/*.h
 declares, and its host-only entry points validate arguments like the
 reference (no GPU compute is called here)."""
 
@@ -13,7 +13,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 
 def header_symbols():
-    txt = (ROOT / "include" / "bmc.h").read_text()
+    txt = "\n".join(h.read_text() for h in sorted((ROOT / "include").glob("*.h")))
     return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(bmc_[a-z_0-9]+)\s*\(", txt, re.M)))
 
 
