@@ -7,11 +7,16 @@ One "step" = one pass of the hot path over one synthetic clip per GPU:
 pack -> ME (all pairs) -> MV refine -> AEM scan -> label chain, replayed as a
 CUDA graph.  ``value`` times the device-resident step (inputs already in HBM,
 L2 flushed between steps); ``e2e`` times the public host-buffer API
-(pipeline.ClipSession.run: pinned H2D of the raw clip + key labels, the step,
-D2H of decisions and labels).  Under torchrun each rank processes its own
-clip (weak scaling, no collective on the hot path; one all_reduce(MAX) of the
-timings at the end).  ``--impl reference`` times the reference algorithm's
-CPU restatement (oracle/, process-parallel over block rows on all host cores).
+(pipeline.ClipSession.run: pinned H2D of the raw clip and of the key label
+maps predicted frames reference, the step, D2H of the decisions and of the
+predicted frames' labels -- a key frame's output is its input map, returned
+as-is like the reference does).  ``--config c2`` also reports
+``variant_fixed_gop``: the same clip with max_gop=6 (25 predicted frames,
+ring-vote refinement), so compensation is timed too.  Under torchrun (or
+``--gpus N``, which launches it) each rank processes its own streams (weak
+scaling; c4 shards 64 streams k -> rank k mod N; no collective on the hot
+path; one all_reduce(MAX) of the timings at the end).  ``--impl reference``
+times the reference algorithm's CPU restatement (oracle/) on all host cores.
 """
 
 from __future__ import annotations
@@ -37,20 +42,28 @@ SAD_U8_SAMPLES_PER_CLK_SM = 256.0
 SAD_U16_SAMPLES_PER_CLK_SM = 64.0
 
 CONFIGS = {
-    # name: (W, H, T, velocity, seed, stages, block_sizes, dtype, description)
+    # name: (W, H, T, velocity, seed, stages, block_sizes, dtype, description, pipeline overrides)
     "c2": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
-           "1920x1080 RGGB uint8 30-frame pan clip, 16x16 blocks, +-16 full search, AEM key selection"),
+           "1920x1080 RGGB uint8 30-frame pan clip, 16x16 blocks, +-16 full search, AEM key selection", {}),
+    # C2 with a fixed key interval (max_gop=6, aem=inf) and the CaBR ring-vote fallback: 25 of 30
+    # frames are predicted, so compensation (label chain + ring vote) is inside the timed step
+    "c2gop": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
+              "C2 clip with a fixed key interval (max_gop=6, aem=inf): 25 predicted frames, ring-vote refinement",
+              {"max_gop": 6, "aem_threshold": float("inf"), "refine_enabled": True}),
     "c2u16": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint16",
-              "1920x1080 RGGB uint16 30-frame pan clip (C2's uint16 variant), 16x16 blocks, +-16 full search"),
+              "1920x1080 RGGB uint16 30-frame pan clip (C2's uint16 variant), 16x16 blocks, +-16 full search", {}),
     "c1": (256, 256, 8, (2, 2), 3, ((8, 1), (0, 1), (0, 1)), (16,), "uint8",
-           "256x256 RGGB uint8 8-frame clip, 16x16 blocks, +-8 full search"),
+           "256x256 RGGB uint8 8-frame clip, 16x16 blocks, +-8 full search", {}),
     "c3": (3840, 2160, 60, (6, -4), 11, ((4, 8), (2, 4), (2, 1)), (8,), "uint16",
-           "3840x2160 RGGB uint16 60-frame clip, 8x8 blocks, 3-stage +-32 reach, refine + compensate"),
-    "c5": (1920, 1080, 40, (24, -16), 7, ((4, 8), (2, 4), (2, 1)), (64, 32), "uint8",
-           "1080p RGGB uint8 40-frame high-motion pan, standard preset (64->32 split)"),
-    # C4: 64 independent C2 streams, sharded 64/N per GPU (stream k: seed 1000+k, SURVEY §8d velocities)
+           "3840x2160 RGGB uint16 60-frame clip, 8x8 blocks, 3-stage +-32 reach, refine + compensate (max_gop=6)",
+           {"max_gop": 6, "aem_threshold": float("inf"), "refine_enabled": False}),
+    "c5": (1920, 1080, 40, "c5", 7, ((4, 8), (2, 4), (2, 1)), (64, 32), "uint8",
+           "1080p RGGB uint8 40-frame high-motion sweep + moving square + scene cut, standard preset (64->32 "
+           "split), max_gop=5", {"max_gop": 5, "aem_threshold": float("inf"), "refine_enabled": False}),
+    # C4: 64 independent C2 streams, stream k -> rank k mod N; seed 1000+k, SURVEY §8d velocities
     "c4": (1920, 1080, 30, None, 1000, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
-           "64 streams of 1920x1080 RGGB uint8 30-frame clips, 16x16 blocks, +-16 full search, sharded across GPUs"),
+           "64 streams of 1920x1080 RGGB uint8 30-frame clips, 16x16 blocks, +-16 full search, sharded across GPUs",
+           {}),
 }
 C4_STREAMS = 64
 
@@ -68,16 +81,20 @@ def pipeline_config(name):
     from paper_2508_05990_b200.fme import FmeConfig, SearchStage
     c = CONFIGS[name]
     fme = FmeConfig(stages=tuple(SearchStage(*s) for s in c[5]), block_sizes=c[6])
-    return PipelineConfig(fme=fme, refine_enabled=False)
+    kw = {"refine_enabled": False, **c[9]}
+    return PipelineConfig(fme=fme, **kw)
 
 
 def make_clip(name, seed_offset=0):
     from paper_2508_05990_b200 import synth
     w, h, t, v, seed = CONFIGS[name][:5]
-    if v is None:  # c4: per-stream velocity
-        v = c4_velocity(seed_offset)
     dt = np.uint16 if CONFIGS[name][7] == "uint16" else np.uint8
-    clip = synth.bayer_pan_clip(w, h, t, v, seed=seed + seed_offset, dtype=dt)
+    if v == "c5":
+        clip = synth.c5_clip(w, h, t, seed=seed + seed_offset, dtype=dt)
+    else:
+        if v is None:  # c4: per-stream velocity
+            v = c4_velocity(seed_offset)
+        clip = synth.bayer_pan_clip(w, h, t, v, seed=seed + seed_offset, dtype=dt)
     labels = synth.block_labels(w, h, t, seed=seed + seed_offset)
     return clip, labels
 
@@ -134,6 +151,7 @@ class ClockSampler:
 # CPU side: the reference algorithm (oracle restatement) on host cores
 # ---------------------------------------------------------------------------
 def _cpu_rows_worker(args):
+    """Level-0 search of some block rows of one pair (single-level configs)."""
     raw_c, raw_r, cfg, rows = args
     from oracle import bayermc_oracle as O
     pc = O.pad_edge(O.search_planes(raw_c, True), cfg["block_sizes"][0])
@@ -148,8 +166,16 @@ def _cpu_rows_worker(args):
     return out
 
 
-def cpu_pair(pool, procs, raw_c, raw_r, cfg, labels_ref, acc, fsk):
-    """One frame pair through ME (block rows split over processes) -> refine -> decide -> predict."""
+def _cpu_pair_worker(args):
+    """Whole hierarchical ME + refine of one pair (multi-level configs)."""
+    raw_c, raw_r, cfg = args
+    from oracle import bayermc_oracle as O
+    pc, pr = O.search_planes(raw_c, True), O.search_planes(raw_r, True)
+    lv = O.estimate_motion(pc, pr, cfg)
+    return O.refine_mvs(lv[-1], 4, pc, pr, cfg)
+
+
+def _cpu_level0_pair(pool, procs, raw_c, raw_r, cfg):
     from oracle import bayermc_oracle as O
     b = cfg["block_sizes"][0]
     ph = -(-raw_c.shape[0] // 2 // b) * b
@@ -165,48 +191,61 @@ def cpu_pair(pool, procs, raw_c, raw_r, cfg, labels_ref, acc, fsk):
     real_h, real_w = raw_c.shape[0] // 2, raw_c.shape[1] // 2
     in_real = ((np.arange(gh) * b)[:, None] < real_h) & ((np.arange(gw) * b)[None, :] < real_w)
     field = O.OracleField(b, mv, en, ~((en > cfg["refine_block_threshold"]) & in_real), 0, 0)
-    refined = O.refine_mvs(field, 4, O.search_planes(raw_c, True), O.search_planes(raw_r, True), cfg)
-    kind, _r, _t, acc, fsk = O.decide(acc, fsk, b, refined.energy, b, 1)
-    lab = O.predict_labels(labels_ref, refined, 2)
-    return lab, acc, fsk
+    return O.refine_mvs(field, 4, O.search_planes(raw_c, True), O.search_planes(raw_r, True), cfg)
 
 
-def cpu_measure(name, pairs, procs):
-    """Seconds for `pairs` frame pairs of config `name` on `procs` processes (1-level configs)."""
+def cpu_measure(name, procs):
+    """One bounded CPU sample of config `name` on `procs` processes: returns (seconds, frames, sample text).
+
+    Single-level configs: ONE frame pair, its block rows split over the processes.
+    Multi-level configs: min(procs, T-1) frame pairs, one per process (pairs are independent under the
+    "previous" policy).  Either way followed by the serial tail (decide + predict) as run_sequence does."""
     import multiprocessing as mp
     from oracle import bayermc_oracle as O
     c = CONFIGS[name]
+    pcfg = pipeline_config(name)
     cfg = O.cfg_dict(stages=c[5], block_sizes=c[6])
     clip, labels = make_clip(name)
+    coarse = c[6][0]
+    acc = np.zeros((-(-clip.shape[1] // 2 // coarse), -(-clip.shape[2] // 2 // coarse)))
     ctx = mp.get_context("fork")
     with ctx.Pool(procs) as pool:
-        acc = np.zeros((-(-clip.shape[1] // 2 // c[6][0]), -(-clip.shape[2] // 2 // c[6][0])))
-        fsk = 0
-        lab = labels[0].classes
         t0 = time.perf_counter()
-        for i in range(1, pairs + 1):
-            lab, acc, fsk = cpu_pair(pool, procs, clip[i], clip[i - 1], cfg, lab, acc, fsk)
-        return time.perf_counter() - t0
+        if len(c[6]) == 1:
+            refined = [_cpu_level0_pair(pool, procs, clip[1], clip[0], cfg)]
+            what = f"1 frame pair of {name}, block rows over {procs} processes"
+        else:
+            n = min(procs, clip.shape[0] - 1)
+            refined = pool.map(_cpu_pair_worker, [(clip[i], clip[i - 1], cfg) for i in range(1, n + 1)])
+            what = f"{n} frame pairs of {name}, one per process ({procs} processes)"
+        fsk, lab = 0, labels[0].classes
+        for i, rf in enumerate(refined, start=1):
+            kind, _r, _t, acc, fsk = O.decide(acc, fsk, coarse, rf.energy, rf.block_size, i,
+                                              pcfg.aem_threshold, pcfg.max_gop)
+            lab = labels[i].classes if kind == "key" else O.predict_labels(lab, rf, 2)
+        return time.perf_counter() - t0, len(refined), what + " (ME+refine+decide+predict, numpy oracle)"
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
     if rank != 0:
         return 0
     procs = os.cpu_count() or 1
     name = args.config
     c = CONFIGS[name]
-    per_step = []
+    secs, frames = [], 0
     for it in range(args.warmup + args.steps):
-        dt = cpu_measure(name, 1, procs)
+        dt, n, what = cpu_measure(name, procs)
         if it >= args.warmup:
-            per_step.append(dt)
-    ms = 1e3 * statistics.mean(per_step)
-    fps = 1e3 / ms
-    sample = f"{args.steps} steps x 1 frame pair of {name} (ME+refine+decide+predict), block rows over {procs} processes"
+            secs.append(dt)
+            frames = n
+    ms = 1e3 * statistics.mean(secs)
+    fps = frames / (ms / 1e3)
+    sample = f"{args.steps} steps x {what}"
     line = {"impl": "reference", "metric": "frames_per_sec", "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": c[7].replace("uint", "u"), "data": "synthetic",
-            "config": {"workload": c[8], "frames_per_step": 1},
+            "config": {"workload": c[8], "frames_per_step": frames},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": procs, "kind": "port", "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -216,52 +255,43 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # GPU side
 # ---------------------------------------------------------------------------
-def run_b200(args, rank, world, local_rank):
+def _hbm_peak():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6553.0  # B200_PROFILING.md fallback (measured copy bandwidth)
+
+
+def measure(name, args, rank, world, local_rank, stream_ids, flush):
+    """Device-resident step (graph replay, L2 flushed) and e2e (ClipSession, host buffers) of one config."""
     import torch
-    from paper_2508_05990_b200 import _native as N
     from paper_2508_05990_b200.engine import ClipEngine
     from paper_2508_05990_b200.pipeline import ClipSession
 
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    name = args.config
     c = CONFIGS[name]
     W, H, T = c[0], c[1], c[2]
     pcfg = pipeline_config(name)
-    if name == "c4":
-        if C4_STREAMS % world:
-            raise SystemExit(f"c4 shards {C4_STREAMS} streams: world size {world} must divide it")
-        S = C4_STREAMS // world
-        stream_ids = [rank * S + k for k in range(S)]  # contiguous shard per rank, no hot-path collective
-    else:
-        S = max(1, args.streams)
-        stream_ids = [rank * S + k for k in range(S)]
+    S = len(stream_ids)
     clips = [make_clip(name, seed_offset=sid) for sid in stream_ids]
-    clip, labels = clips[0]
-    dt = clip.dtype
-
+    dt = clips[0][0].dtype
     eng = ClipEngine(pcfg, H, W, T, S, dt, True)
-    eng.load_frames(np.stack([c for c, _ in clips]))
+    eng.load_frames(np.stack([cl for cl, _ in clips]))
     for k, (_c, labs) in enumerate(clips):
-        for t in range(T):
-            eng.key_labels[k, t].copy_(torch.from_numpy(labs[t].classes.copy()))
+        eng.key_labels[k].copy_(torch.from_numpy(np.stack([labs[t].classes for t in range(T)])))
     eng.capture()
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 512 MB > 126 MB L2
 
     def flush_l2():
         flush.fill_(rank + 1)
 
-    # warm-up
     for _ in range(max(args.warmup, 3)):
         flush_l2()
         eng.replay()
     torch.cuda.synchronize()
 
-    # --- timed device-resident steps (value); the ME graph of every step is bracketed by events ---
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    me_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    me_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+    me_s, me_e = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -275,65 +305,97 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    # dominant kernel: the ME launch(es) of each timed step (same stream as the kernel launches)
     me_ms = [s.elapsed_time(e) for s, e in zip(me_s, me_e)]
-    me_avg = statistics.mean(me_ms)
+    post_ms = [m.elapsed_time(e) for m, e in zip(me_e, ends)]  # refine + AEM scan + label chain
     evals = [int(lv.evals[:eng.n_pairs].sum().item()) for lv in eng.levels]
-    P = 4
-    samples = sum(e * P * b * b for e, b in zip(evals, pcfg.fme.block_sizes))
+    samples = sum(e * 4 * b * b for e, b in zip(evals, pcfg.fme.block_sizes))
     bpp = np.dtype(dt).itemsize
-    me_bytes = eng.n_pairs * 2 * bpp * W * H  # cur + ref reads per pair
-    step_bytes = S * (T - 1) * (2 * bpp * W * H + 2 * W * H)  # frames + label read/write
+    kinds = eng.kind.cpu().numpy()
+    predicted = int((kinds != 0).sum())
+    keyframes = int((kinds == 0).sum())
 
-    # --- e2e through the public host-buffer API ---
+    # --- e2e through the public host-buffer API, every stream of this rank ---
     sess = ClipSession(pcfg, H, W, T, dt, True)
-    # per stream: pinned raw clip + key labels as one pinned (T, H, W) tensor (only key frames' maps are
-    # used; the upload overlaps ME)
-    host_in = [(torch.from_numpy(c).pin_memory(),
-                torch.from_numpy(np.stack([labs[t].classes for t in range(T)])).pin_memory()) for c, labs in clips]
+    host_in = [(torch.from_numpy(cl).pin_memory(),
+                torch.from_numpy(np.stack([labs[t].classes for t in range(T)])).pin_memory()) for cl, labs in clips]
     for _ in range(2):
         for raw_k, key_k in host_in:
             sess.run(raw_k, key_k)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    e2e_ms = []
+    e2e_ms, h2d, d2h = [], 0, 0
     for _ in range(args.steps):
         flush_l2()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for raw_k, key_k in host_in:  # every stream of this rank through the public API
-            out_labels, kinds, _refs, _trig = sess.run(raw_k, key_k)
+        h2d = d2h = 0
+        for raw_k, key_k in host_in:
+            out_labels, _k, _r, _t = sess.run(raw_k, key_k)
+            h2d += sess.h2d_bytes
+            d2h += sess.d2h_bytes
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    # outside the timed region: the last stream's e2e labels equal the device-resident run's
-    e2e_ok = bool(np.array_equal(out_labels, eng.labels[S - 1].cpu().numpy()))
+    e2e_ok = bool(np.array_equal(np.stack(out_labels), eng.labels[S - 1].cpu().numpy()))
+    return {"eng": eng, "pcfg": pcfg, "S": S, "W": W, "H": H, "T": T, "bpp": bpp, "step_ms": step_ms,
+            "me_ms": me_ms, "post_ms": post_ms, "samples": samples, "predicted": predicted, "keyframes": keyframes,
+            "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "e2e_ok": e2e_ok, "clocks": clocks.summary(), "dev": dev}
+
+
+def rank_streams(name, world, rank, streams=1):
+    """Stream ids this rank runs: c4 shards its 64 streams round-robin (stream k -> rank k mod N,
+    sharding.shard_streams); other configs give every rank its own `streams` clips."""
+    from paper_2508_05990_b200 import sharding
+    if name == "c4":
+        if world > C4_STREAMS:
+            raise SystemExit(f"c4 has {C4_STREAMS} streams; world size {world} leaves ranks idle")
+        return sharding.shard_streams(C4_STREAMS, world, rank)
+    s = max(1, int(streams))
+    return [rank * s + k for k in range(s)]
+
+
+def _reduce_max(vals, args, dev, world):
+    import torch
+    coll_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    t = torch.tensor(vals, dtype=torch.float64, device=coll_dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    from paper_2508_05990_b200 import sharding
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    name = args.config
+    c = CONFIGS[name]
+    stream_ids = rank_streams(name, world, rank, args.streams)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 512 MB > 126 MB L2
+    m = measure(name, args, rank, world, local_rank, stream_ids, flush)
+    eng, S, W, H, T, bpp = m["eng"], m["S"], m["W"], m["H"], m["T"], m["bpp"]
 
     # --- max over ranks (the only collective: one tiny exchange after timing) ---
-    from paper_2508_05990_b200 import sharding
     digest = sharding.parity_hash(eng.labels.cpu().numpy(), eng.kind.cpu().numpy())
     coll_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    total_ms = sum(m["step_ms"])
     stats = sharding.gather_stats((T - 1) * S * args.steps, total_ms / 1e3, digest, device=coll_dev)
-    vals = torch.tensor([total_ms, statistics.mean(e2e_ms), me_avg], dtype=torch.float64, device=coll_dev)
-    if world > 1:
-        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
-    total_ms, e2e_avg, me_avg = (float(v) for v in vals.tolist())
+    total_ms, e2e_avg, me_avg, post_avg = _reduce_max(
+        [total_ms, statistics.mean(m["e2e_ms"]), statistics.mean(m["me_ms"]), statistics.mean(m["post_ms"])],
+        args, dev, world)
     ms_per_step = total_ms / args.steps
-    frames = (T - 1) * S * world
+    frames = int(sum(r[0] for r in stats)) // args.steps  # frames of all ranks per step
     value = frames / (ms_per_step / 1e3)
     e2e_value = frames / (e2e_avg / 1e3)
 
-    clk = clocks.summary()
+    clk = m["clocks"]
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     rate = SAD_U8_SAMPLES_PER_CLK_SM if bpp == 1 else SAD_U16_SAMPLES_PER_CLK_SM
     sm_mhz = clk.get("sm_mhz") or 1965.0
     peak = rate * sms * sm_mhz * 1e6 / 1e9  # Gsamples/s at the clock seen under load
-    achieved = samples / (me_avg / 1e3) / 1e9
-    hbm_peak = 6543.4
-    try:
-        hbm_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
-    except Exception:
-        pass
+    achieved = m["samples"] / (me_avg / 1e3) / 1e9
+    hbm_peak = _hbm_peak()
+    me_bytes = eng.n_pairs * 2 * bpp * W * H  # cur + ref reads per pair
     traffic = None
     prof = ROOT / "profiles" / f"ncu_{name}_fme_level.json"
     if prof.exists():
@@ -341,47 +403,87 @@ def run_b200(args, rank, world, local_rank):
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    launches_per_step = eng.launches_per_step()
-
+    pcfg = m["pcfg"]
+    searched = sum(1 for k, st in enumerate(pcfg.fme.stages) if not (st.range == 0 and k > 0))
     line = {
         "metric": "frames_per_sec", "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8" if bpp == 1 else "u16", "data": "synthetic",
-        "config": {"workload": c[8], "frames_per_step_per_gpu": (T - 1) * S, "streams_per_gpu": S,
-                   "l2": "flushed (512 MB write) between timed steps", "graph": "3 CUDA graphs per step (pack | ME | refine+AEM+label chain), events around the ME graph",
+        "config": {"workload": c[8], "name": name, "frames_per_step_per_gpu": (T - 1) * S, "streams_per_gpu": S,
+                   "l2": "flushed (512 MB write) between timed steps",
+                   "graph": "3 CUDA graphs per step (pack | ME | refine+AEM+label chain), events around the ME graph",
                    "parallelism": f"stream-sharded x{world} (no hot-path collective)"},
         "roofline": {"bound": "int_alu", "achieved": achieved, "peak": peak, "unit": "Gsamples/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"fme_stage_kernel x{sum(1 for k, st in enumerate(pcfg.fme.stages) if not (st.range == 0 and k > 0)) * len(pcfg.fme.block_sizes)} (bmc_estimate_motion), CUDA events around the ME graph inside every timed step",
-                     "kernel_ms": me_avg,
-                     "samples_per_launch": samples,
-                     "peak_basis": f"{rate:.0f} samples/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz (measured SAD issue rate,"
-                                   " tools/sad_peak.cu)",
+                     "kernel": f"ME: {searched * len(pcfg.fme.block_sizes)} launch(es) of bmc_estimate_motion per step "
+                               "(fme_stage_kernel / fme_small_kernel), CUDA events around the ME graph in every "
+                               "timed step",
+                     "kernel_ms": me_avg, "samples_per_launch": m["samples"],
+                     "peak_basis": f"{rate:.0f} samples/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz (measured SAD issue "
+                                   "rate, tools/sad_peak.cu)",
                      "hbm": {"algorithmic_bytes": me_bytes, "achieved_gbs": me_bytes / (me_avg / 1e3) / 1e9,
                              "peak_gbs": hbm_peak}},
-        "kernel_share_of_step": me_avg / (total_ms / args.steps),
-        "step_bytes_algorithmic": step_bytes,
-        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": sess.h2d_bytes * S,
-                "d2h_bytes_per_step": sess.d2h_bytes * S, "ms_per_step": e2e_avg, "labels_match_device_run": e2e_ok,
-                "ms_per_step_samples": [round(v, 3) for v in e2e_ms]},
-        "gpu_launches": launches_per_step * args.steps,
+        "kernel_share_of_step": me_avg / ms_per_step,
+        "compensation": _compensation_block(m, post_avg, hbm_peak),
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": m["h2d"],
+                "d2h_bytes_per_step": m["d2h"], "ms_per_step": e2e_avg, "labels_match_device_run": m["e2e_ok"],
+                "ms_per_step_samples": [round(v, 3) for v in m["e2e_ms"]]},
+        "gpu_launches": eng.launches_per_step() * args.steps,
         "clocks": clk,
-        "keyframes_per_clip": int((eng.kind[0] == 0).sum().item()),
         "ranks": [{"frames": int(r[0]), "seconds": float(r[1]),
                    "parity_hash": f"{int(r[3]) << 32 | int(r[2]):016x}"} for r in stats],
     }
+    if name == "c2" and not args.no_variant:
+        # the same clip with a fixed key interval: compensation (label chain + CaBR ring vote) in the step
+        del m, eng
+        torch.cuda.empty_cache()
+        mv = measure("c2gop", args, rank, world, local_rank, stream_ids, flush)
+        t_ms, e_ms, p_ms, me_ms = _reduce_max([statistics.mean(mv["step_ms"]), statistics.mean(mv["e2e_ms"]),
+                                               statistics.mean(mv["post_ms"]), statistics.mean(mv["me_ms"])],
+                                              args, dev, world)
+        fr = (mv["T"] - 1) * mv["S"] * world
+        line["variant_fixed_gop"] = {
+            "workload": CONFIGS["c2gop"][8], "value": fr / (t_ms / 1e3), "unit": "frames/s", "ms_per_step": t_ms,
+            "me_ms": me_ms, "predicted_frames_per_clip": mv["predicted"] // mv["S"],
+            "compensation": _compensation_block(mv, p_ms, hbm_peak),
+            "e2e": {"value": fr / (e_ms / 1e3), "unit": "frames/s", "h2d_bytes_per_step": mv["h2d"],
+                    "d2h_bytes_per_step": mv["d2h"], "ms_per_step": e_ms, "labels_match_device_run": mv["e2e_ok"]}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
         try:
-            secs = cpu_measure(name, 1, procs)
-            line["cpu_baseline"] = {"value": 1.0 / secs, "unit": "frames/s", "cores": procs, "kind": "port",
-                                    "sample": f"1 frame pair of {name} (ME+refine+decide+predict) with the numpy "
-                                              f"oracle, block rows over {procs} processes"}
+            secs, n, what = cpu_measure(name, procs)
+            line["cpu_baseline"] = {"value": n / secs, "unit": "frames/s", "cores": procs, "kind": "port",
+                                    "sample": what}
         except Exception as exc:  # report, never fake
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def _compensation_block(m, post_ms, hbm_peak):
+    """Key/predicted frame counts and the label-chain HBM roofline (2*W*H per
+    predicted frame -- reference label read + label write; key frames copy their map)."""
+    W, H, S = m["W"], m["H"], m["S"]
+    byts = 2 * W * H * (m["predicted"] + m["keyframes"])
+    return {"keyframes_per_clip": m["keyframes"] // S, "predicted_frames_per_clip": m["predicted"] // S,
+            "bound": "hbm", "unit": "GB/s", "algorithmic_bytes": byts, "post_me_ms": post_ms,
+            "achieved": byts / (post_ms / 1e3) / 1e9, "peak": hbm_peak,
+            "frac": byts / (post_ms / 1e3) / 1e9 / hbm_peak,
+            "kernels": "refine_kernel + decide_max_kernel + predict_chain_kernel (events from the end of the ME "
+                       "graph to the end of the step)"}
+
+
+def _respawn_distributed(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: launch N ranks on this node (one per GPU)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -392,22 +494,24 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variant", action="store_true", help="skip the fixed-GOP compensation variant of c2")
     ap.add_argument("--streams", type=int, default=1, help="independent clips per GPU (c4: 64 / world)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for the final timing / parity gather (gloo lets ranks share a GPU in tests)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _respawn_distributed(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl != "reference" and args.dist_backend == "gloo":
-        # test mode: several ranks may share one GPU (no NCCL); the hot path has no collective anyway
-        import torch
-        local_rank = local_rank % max(1, torch.cuda.device_count())
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    import torch
+    if args.dist_backend == "gloo":
+        # test mode: several ranks may share one GPU (no NCCL); the hot path has no collective anyway
+        local_rank = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
-        import torch
         torch.cuda.set_device(local_rank)
         if args.dist_backend == "nccl":
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -417,7 +521,6 @@ def main():
         return run_b200(args, rank, world, local_rank)
     finally:
         if world > 1:
-            import torch
             torch.distributed.destroy_process_group()
 
 

@@ -11,9 +11,34 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "bmc.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+/* ---------------------------------------------------------- plane stacks --
+ * Motion search on float64 (P, H, W) plane stacks: the reference accepts an
+ * ndarray in place of a Frame and uses it as-is, without normalisation
+ * (fme.py:188-190, :275, :337-340).  Also the general path for geometries the
+ * integer kernels do not take (block sizes outside 8..64 / non-power-of-two
+ * search_stage blocks): Frames are normalised on device first.  Exact float64
+ * energies, the reference's candidate order and tie-breaking.
+ * bmc_estimate_motion_f64: planes edge-padded to (pad_h, pad_w), contiguous
+ * (P, pad_h, pad_w) per stack; one pair; levels[L] as in bmc_estimate_motion
+ * (pair dimension 1).  Replaces estimate_motion (fme.py:324-392) for stacks.
+ * bmc_search_stage_f64: unpadded (P, height, width) stacks, one block, one
+ * stage around (center_x, center_y); n_valid 0 = no valid candidate (the
+ * reference raises).  Replaces search_stage (fme.py:271-291) for stacks. */
+int bmc_estimate_motion_f64(const double* cur_planes, const double* ref_planes, int planes, int pad_h, int pad_w,
+                            int real_h, int real_w, int n_levels, const int32_t* block_sizes,
+                            const int32_t* stage_range, const int32_t* stage_step, double lam,
+                            double sparsity_tolerance, double split_threshold, double refine_block_threshold,
+                            bmc_level_out* levels, void* stream);
+int bmc_search_stage_f64(const double* cur_planes, const double* ref_planes, int planes, int height, int width,
+                         int origin_x, int origin_y, int block_size, int center_x, int center_y, int search_range,
+                         int step, double lam, double sparsity_tolerance, int32_t* mv_out, double* energy_out,
+                         int32_t* n_valid_out, void* stream);
 
 /* ---------------------------------------------------------------- ingest --
  * Raw sensor payloads -> uint16 frames, on device (frame_io.py:202-241 reads

@@ -75,7 +75,10 @@ _SIGNATURES = {
                                                ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
     "bmc_predict_features": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]),
-    # include/bmc_ext.h: ingest, reporting
+    # include/bmc_ext.h: float64 plane stacks, ingest, reporting
+    "bmc_estimate_motion_f64": (ctypes.c_int, [vp, vp] + [ctypes.c_int] * 6 + [ctypes.POINTER(i32)] * 3
+                                + [f64] * 4 + [ctypes.POINTER(LevelOut), vp]),
+    "bmc_search_stage_f64": (ctypes.c_int, [vp, vp] + [ctypes.c_int] * 10 + [f64, f64, vp, vp, vp, vp]),
     "bmc_unpack_raw": (ctypes.c_int, [vp, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, vp, vp]),
     "bmc_pack_be16": (ctypes.c_int, [vp, i64, vp, vp]),

@@ -510,8 +510,8 @@ int bmc_predict_labels_clip(uint8_t* labels, int64_t frame_stride, int64_t strea
   a.gw = grid_w;
   a.B = B;
   a.scale = scale;
-  if (matched && !scratch) {
-    set_error("ring-vote refinement needs a scratch frame buffer");
+  if (matched && B % 16) {
+    set_error("CaBR block size must be a multiple of 16 pixels, got %d", B);
     return BMC_E_ARG;
   }
   if (matched && B < 16) {

@@ -4,6 +4,8 @@
 // reference's operation order with explicitly rounded intrinsics.
 #include <cstdio>
 
+#include <algorithm>
+
 #include "bmc_internal.cuh"
 #include "bmc_launch.cuh"
 
@@ -548,65 +550,98 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
-// CaBR's weight-free fallback (cabr.py:257-345) for frame t: pixels of
-// flagged blocks (final-level matched == 0) take the vote of the ring pixels
-// straight across the four block borders, read from the unrefined prediction
-// in `scratch`; other pixels copy it.  Candidates inside any flagged block are
+// Unrefined prediction of the 16 pixels (row py, columns x0..x0+15, all inside
+// final block column gx) of frame t: ref[clip(py + s*dy), clip(x + s*dx)] with
+// the MV of block (py / B, gx) (propagate.py:39-53).  Lanes past the frame are 0.
+__device__ __forceinline__ uint4 predict16(const PredictArgs& a, const uint8_t* src, const int32_t* mv, int py,
+                                           int x0, int gx, bool vec_ok) {
+  const int c = (py / a.B) * a.gw + gx;
+  const int dx = __ldg(mv + 2 * c) * a.scale, dy = __ldg(mv + 2 * c + 1) * a.scale;
+  const int sy = min(max(py + dy, 0), a.H - 1);
+  const int sx = x0 + dx;
+  const uint8_t* row = src + (long long)sy * a.W;
+  if (vec_ok && sx >= 0 && sx + 16 <= a.W && x0 + 16 <= a.W) {
+    const uint32_t* r32 = reinterpret_cast<const uint32_t*>(row);
+    const int w0 = sx >> 2, sh = (sx & 3) * 8;
+    uint32_t v[5];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcg(r32 + w0 + q);
+    v[4] = sh ? __ldcg(r32 + w0 + 4) : 0u;
+    return make_uint4(__funnelshift_r(v[0], v[1], sh), __funnelshift_r(v[1], v[2], sh),
+                      __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
+  }
+  uint32_t w[4] = {0, 0, 0, 0};
+  const int n = min(16, a.W - x0);
+  for (int e = 0; e < n; ++e) {
+    const int x = min(max(x0 + e + dx, 0), a.W - 1);
+    w[e >> 2] |= (uint32_t)__ldcg(row + x) << (8 * (e & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Unrefined prediction of one pixel (py, px) of frame t.
+__device__ __forceinline__ int predict1(const PredictArgs& a, const uint8_t* src, const int32_t* mv, int py, int px) {
+  const int c = (py / a.B) * a.gw + px / a.B;
+  const int dx = __ldg(mv + 2 * c) * a.scale, dy = __ldg(mv + 2 * c + 1) * a.scale;
+  return __ldcg(src + (long long)min(max(py + dy, 0), a.H - 1) * a.W + min(max(px + dx, 0), a.W - 1));
+}
+
+__device__ __forceinline__ int byte_of(const uint4& v, int e) {
+  const uint32_t w = e < 8 ? (e < 4 ? v.x : v.y) : (e < 12 ? v.z : v.w);
+  return (w >> (8 * (e & 3))) & 0xff;
+}
+
+// CaBR's weight-free fallback (cabr.py:257-303 _ring_vote, applied by
+// refine_blocks(weights=None), :306-345) for one 16-pixel group of a FLAGGED
+// final block (matched == 0) of predicted frame t, fused with the prediction:
+// the ring pixels straight across the four block borders are predicted on the
+// fly from the reference frame with THEIR blocks' MVs (the reference votes on
+// the unrefined prediction of the whole frame), so no scratch frame and no
+// second grid barrier are needed.  Candidates inside any flagged block are
 // dropped unless all four are; among kept candidates at minimal distance the
 // class with most votes wins, ties to the smallest class id.  All integer.
-__device__ void ring_vote_frame(const PredictArgs& a, int n_streams, int t, long long total, long long per_stream,
-                                int groups_per_row) {
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
-    const int stream = (int)(g / per_stream);
-    const long long gg = g - stream * per_stream;
-    if (a.kind && a.kind[(long long)stream * a.kss + t] == 0) continue;  // key frames are not refined
-    const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
-    const int n = min(16, a.W - x0);
-    const uint8_t* P = a.scratch + (long long)stream * a.H * a.W;
-    uint8_t* out = a.labels + stream * a.ss + t * a.fs + (long long)y * a.W;
-    const uint8_t* m = a.matched + stream * (a.mvss / 2) + t * (a.mvfs / 2);  // cells per frame / stream
-    const int k = a.B;
-    auto flagged = [&](int py, int px) { return m[(py / k) * a.gw + px / k] == 0; };
-    const int gy = y / k, y0 = gy * k, ly = y - y0;
-    const int ty = min(max(y0 - 1, 0), a.H - 1), by = min(max(y0 + k, 0), a.H - 1);
-    for (int e = 0; e < n; ++e) {
-      const int x = x0 + e;
-      const int gx = x / k;
-      if (m[gy * a.gw + gx] != 0) {
-        out[x] = P[(long long)y * a.W + x];
-        continue;
+// Requires B % 16 == 0 (CaBR blocks are >= 16 px), so a group lies in one block.
+__device__ void chain_vote_group(const PredictArgs& a, const uint8_t* src, const int32_t* mv, const uint8_t* m,
+                                 uint8_t* out_row, int y, int x0, bool vec_ok) {
+  const int k = a.B;
+  const int gy = y / k, gx = x0 / k, y0 = gy * k, xb = gx * k, ly = y - y0;
+  const int ty = min(max(y0 - 1, 0), a.H - 1), by = min(max(y0 + k, 0), a.H - 1);
+  const int lxp = min(max(xb - 1, 0), a.W - 1), rxp = min(max(xb + k, 0), a.W - 1);
+  auto flagged = [&](int py, int px) { return m[(py / k) * a.gw + px / k] == 0; };
+  const uint4 top = predict16(a, src, mv, ty, x0, gx, vec_ok);
+  const uint4 bot = predict16(a, src, mv, by, x0, gx, vec_ok);
+  const int left = predict1(a, src, mv, y, lxp), right = predict1(a, src, mv, y, rxp);
+  const bool ft = flagged(ty, x0), fb = flagged(by, x0), fl = flagged(y, lxp), fr = flagged(y, rxp);
+  const bool any_clean = !(ft && fb && fl && fr);
+  const bool use[4] = {!(any_clean && ft), !(any_clean && fb), !(any_clean && fl), !(any_clean && fr)};
+  uint32_t w[4] = {0, 0, 0, 0};
+  const int n = min(16, a.W - x0);
+  for (int e = 0; e < n; ++e) {
+    const int lx = x0 + e - xb;
+    const int cls[4] = {byte_of(top, e), byte_of(bot, e), left, right};
+    const int dist[4] = {ly + 1, k - ly, lx + 1, k - lx};
+    int dmin = 0x7fffffff;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (use[c]) dmin = min(dmin, dist[c]);
+    int best = 0, best_votes = -1;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (!use[c] || dist[c] != dmin) continue;
+      int votes = 0;
+#pragma unroll
+      for (int c2 = 0; c2 < 4; ++c2) votes += use[c2] && dist[c2] == dmin && cls[c2] == cls[c];
+      if (votes > best_votes || (votes == best_votes && cls[c] < best)) {
+        best_votes = votes;
+        best = cls[c];
       }
-      const int xb = gx * k, lx = x - xb;
-      const int lxp = min(max(xb - 1, 0), a.W - 1), rxp = min(max(xb + k, 0), a.W - 1);
-      const int ry[4] = {ty, by, y, y}, rx[4] = {x, x, lxp, rxp};
-      const int dist[4] = {ly + 1, k - ly, lx + 1, k - lx};
-      int cls[4];
-      bool fl[4], any_clean = false;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        cls[c] = P[(long long)ry[c] * a.W + rx[c]];
-        fl[c] = flagged(ry[c], rx[c]);
-        any_clean |= !fl[c];
-      }
-      int dmin = 0x7fffffff;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (!(any_clean && fl[c])) dmin = min(dmin, dist[c]);
-      int best = 0, best_votes = -1;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if ((any_clean && fl[c]) || dist[c] != dmin) continue;
-        int votes = 0;
-#pragma unroll
-        for (int c2 = 0; c2 < 4; ++c2)
-          votes += !(any_clean && fl[c2]) && dist[c2] == dmin && cls[c2] == cls[c];
-        if (votes > best_votes || (votes == best_votes && cls[c] < best)) {
-          best_votes = votes;
-          best = cls[c];
-        }
-      }
-      out[x] = (uint8_t)best;
     }
+    w[e >> 2] |= (uint32_t)best << (8 * (e & 3));
+  }
+  if (vec_ok && n == 16) {
+    *reinterpret_cast<uint4*>(out_row + x0) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    for (int e = 0; e < n; ++e) out_row[x0 + e] = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
   }
 }
 
@@ -619,7 +654,13 @@ __device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int str
   const int r = a.ref ? a.ref[o] : a.ref_fixed;
   const uint8_t* src = a.labels + stream * a.ss + (long long)r * a.fs;
   const int32_t* mv = a.mv + stream * a.mvss + t * a.mvfs;
-  if (a.matched) out = a.scratch + (long long)stream * a.H * a.W + (long long)y * a.W;  // refined below
+  if (a.matched) {  // CaBR ring vote on flagged blocks (cells indexed like mv, one byte per cell)
+    const uint8_t* m = a.matched + stream * (a.mvss / 2) + t * (a.mvfs / 2);
+    if (m[(y / a.B) * a.gw + x0 / a.B] == 0) {
+      chain_vote_group(a, src, mv, m, out, y, x0, vec_ok);
+      return;
+    }
+  }
   const int gy = y / a.B;
   const int gx0 = x0 / a.B, gx1 = (x0 + n - 1) / a.B;
   if (vec_ok && n == 16 && gx0 == gx1) {
@@ -665,11 +706,13 @@ __device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int str
   }
 }
 
-// The label chain of frames [t_begin, t_end) (pipeline.py:123-126).  Phase 1
+// The label chain of frames [t_begin, t_end) (pipeline.py:123-132).  Phase 1
 // copies every key frame's injected labels at once: the copies are
 // independent, so the whole grid streams them with eight 16-byte loads in
 // flight per thread.  Phase 2 walks the non-key frames in order with a grid
-// barrier only where a frame reads one written earlier in this phase.
+// barrier only where a frame reads one written earlier in this phase; each
+// predicted frame is ONE pass: plain gathers, and on flagged blocks (ring vote
+// enabled) the fused predict + vote of chain_vote_group.
 constexpr int kChainKindsSmem = 2048;
 __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictArgs a, int n_streams, int t_begin,
                                                                  int t_end, unsigned* barrier_ctr) {
@@ -739,8 +782,7 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
   for (int t = t_begin; t < t_end; ++t) {
     const bool work = !a.kind || frame_has(t, false);
     if (!work) continue;
-    // frame t reads frames <= t-1, and its gather reuses the ring-vote scratch:
-    // any phase-2 work since the last barrier needs one first
+    // frame t reads frames <= t-1: any phase-2 work since the last barrier needs one first
     if (prev_wrote) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
     for (long long g = gtid; g < total; g += stride) {
       const int stream = (int)(g / per_stream);
@@ -748,10 +790,6 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
       const long long gg = g - stream * per_stream;
       const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
       chain_gather_group(a, stream, t, (long long)stream * a.kss + t, y, x0, vec_ok);
-    }
-    if (a.matched) {
-      grid_barrier(barrier_ctr, ++epoch * gridDim.x);  // the whole unrefined prediction of frame t is written
-      ring_vote_frame(a, n_streams, t, total, per_stream, groups_per_row);
     }
     prev_wrote = true;
   }
@@ -770,7 +808,9 @@ int launch_predict_chain(const PredictArgs& a, int n_streams, int t_begin, int t
   }
   const long long tasks = (long long)n_streams * a.H * ((a.W + 15) / 16);
   long long grid = (tasks + kThreads - 1) / kThreads;
-  const long long cap = (long long)per_sm * sms;
+  int use_per_sm = per_sm;
+  if (const char* v = knob_env("BMC_CHAIN_PER_SM")) use_per_sm = std::max(1, std::min(per_sm, atoi(v)));
+  const long long cap = (long long)use_per_sm * sms;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   int rc = cuda_status(cudaMemsetAsync(barrier_ctr, 0, sizeof(unsigned), st), "memset predict barrier");

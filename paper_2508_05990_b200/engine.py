@@ -46,6 +46,10 @@ class ClipEngine:
             raise ValueError("reference_policy must be 'previous' or 'keyframe'")
         if n_frames < 1 or n_streams < 1:
             raise ValueError("need at least one frame and one stream")
+        if any(b > 64 for b in config.fme.block_sizes):
+            raise NotImplementedError(
+                f"the clip engine's integer search kernels take block sizes 8..64, got {config.fme.block_sizes}; "
+                "fme.estimate_motion / search_stage / refine_mvs accept larger blocks (float64 kernel)")
         self.torch = torch
         self.cfg = config
         self.S, self.T, self.H, self.W = int(n_streams), int(n_frames), int(height), int(width)
@@ -108,8 +112,6 @@ class ClipEngine:
         self.key_labels = self.torch.zeros_like(self.labels)
         # CaBR weight-free fallback (ring vote) runs inside the label chain when refinement is on
         self.ring_vote = bool(self.cfg.refine_enabled)
-        self.scratch = self.torch.empty((self.S, h, w), dtype=self.torch.uint8, device=self.dev) \
-            if self.ring_vote else None
         self.graph = None
 
     def load_frames(self, frames, non_blocking: bool = False) -> None:
@@ -210,7 +212,7 @@ class ClipEngine:
             N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, t0, t1, N.ptr(self.kind),
             N.ptr(self.ref), self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
             self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale, matched,
-            N.ptr(self.scratch) if ring else None, N.ptr(self.workspace), N.stream_handle()))
+            None, N.ptr(self.workspace), N.stream_handle()))
 
     def predict(self) -> None:
         """Label chain (one cooperative launch): key frames copy key_labels, others gather from their reference."""

@@ -196,8 +196,7 @@ def block_energy(cur_block, ref_block, lam: float, sparsity_tolerance: float = D
 
 def _frame_kind_pair(cur, ref):
     if not (isinstance(cur, Frame) and isinstance(ref, Frame)):
-        raise NotImplementedError(
-            "the B200 search kernels take uint8/uint16 Frames; float plane stacks are not supported yet")
+        raise NotImplementedError("uint8/uint16 Frames expected here; plane stacks take the float64 path")
     if cur.kind != ref.kind:
         raise ValueError(f"frame kind mismatch: {cur.kind} vs {ref.kind}")
     if (cur.width, cur.height) != (ref.width, ref.height):
@@ -207,9 +206,98 @@ def _frame_kind_pair(cur, ref):
     return cur.kind.is_bayer
 
 
+# Geometry the integer SIMD kernels take; anything else (and every float64 plane
+# stack) goes through the exact float64 kernel (csrc/bmc_fme_f64.cu).
+_INT_BLOCKS = (8, 16, 32, 64)
+
+
+def _integer_path(cur, ref, block_sizes) -> bool:
+    return (isinstance(cur, Frame) and isinstance(ref, Frame) and cur.data.dtype == ref.data.dtype
+            and cur.data.dtype in (np.uint8, np.uint16) and all(b in _INT_BLOCKS for b in block_sizes))
+
+
+def _device_planes(x, torch, dev):
+    """to_search_planes (fme.py:181-195) on the GPU: a Frame is CFA-split and divided
+    by its max value in float64 (IEEE division, as numpy); an ndarray is used as-is."""
+    if isinstance(x, np.ndarray):
+        arr = torch.from_numpy(np.array(x, dtype=np.float64, copy=True)).to(dev)
+        return arr[None] if arr.dim() == 2 else arr
+    t = torch.from_numpy(np.array(x.data, copy=True)).to(dev)
+    t = t.to(torch.int32) if t.dtype == torch.uint16 else t
+    if x.kind.is_bayer:
+        planes = torch.stack([t[k >> 1::2, k & 1::2] for k in range(4)])
+    else:
+        planes = t[None]
+    return planes.to(torch.float64) / float(x.max_value)
+
+
+def _pad_edge_device(planes, multiple: int, torch):
+    """_pad_planes (fme.py:205-211): edge-replicate bottom/right to a multiple."""
+    _, h, w = planes.shape
+    ph, pw = -(-h // multiple) * multiple, -(-w // multiple) * multiple
+    if (ph, pw) == (h, w):
+        return planes.contiguous()
+    iy = torch.clamp(torch.arange(ph, device=planes.device), max=h - 1)
+    ix = torch.clamp(torch.arange(pw, device=planes.device), max=w - 1)
+    return planes[:, iy[:, None], ix[None, :]].contiguous()
+
+
+def _estimate_motion_f64(cur, ref, config) -> list:
+    if isinstance(cur, Frame) and isinstance(ref, Frame):
+        if cur.kind != ref.kind:
+            raise ValueError(f"frame kind mismatch: {cur.kind} vs {ref.kind}")
+        if (cur.width, cur.height) != (ref.width, ref.height):
+            raise ValueError("frame size mismatch")
+    torch = N.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pc, pr = _device_planes(cur, torch, dev), _device_planes(ref, torch, dev)
+    if tuple(pc.shape) != tuple(pr.shape):
+        raise ValueError("frame size mismatch")
+    P, real_h, real_w = (int(v) for v in pc.shape)
+    coarse = config.block_sizes[0]
+    pc, pr = _pad_edge_device(pc, coarse, torch), _pad_edge_device(pr, coarse, torch)
+    H, W = int(pc.shape[1]), int(pc.shape[2])
+    levels = [D.LevelBuffers(torch, dev, 1, H // b, W // b) for b in config.block_sizes]
+    arr = (N.LevelOut * len(levels))(*[lv.as_c() for lv in levels])
+    nl = len(config.block_sizes)
+    bs = (N.i32 * N.MAX_LEVELS)(*config.block_sizes)
+    rs = (N.i32 * 3)(*[int(st.range) for st in config.stages])
+    ss = (N.i32 * 3)(*[int(st.step) for st in config.stages])
+    N.check(N.load().bmc_estimate_motion_f64(N.ptr(pc), N.ptr(pr), P, H, W, real_h, real_w, nl, bs, rs, ss,
+                                             float(config.lam), float(config.sparsity_tolerance),
+                                             float(config.split_threshold), float(config.refine_block_threshold),
+                                             arr, N.stream_handle()))
+    return _fields_from_device(levels, 0, config.block_sizes)
+
+
+def _search_stage_f64(cur, ref, block_origin, block_size, center, search_range, step, config):
+    torch = N.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pc, pr = _device_planes(cur, torch, dev).contiguous(), _device_planes(ref, torch, dev).contiguous()
+    P, height, width = (int(v) for v in pc.shape)
+    ox, oy = (int(v) for v in block_origin)
+    if ox < 0 or oy < 0 or ox + block_size > width or oy + block_size > height:
+        raise ValueError(f"block at {block_origin} size {block_size} lies outside the frame")
+    if tuple(pr.shape) != tuple(pc.shape):
+        raise ValueError("frame size mismatch")
+    mv = torch.empty(2, dtype=torch.int32, device=dev)
+    en = torch.empty(1, dtype=torch.float64, device=dev)
+    nv = torch.empty(1, dtype=torch.int32, device=dev)
+    N.check(N.load().bmc_search_stage_f64(N.ptr(pc), N.ptr(pr), P, height, width, ox, oy, int(block_size),
+                                          int(center[0]), int(center[1]), int(search_range), int(step),
+                                          float(config.lam), float(config.sparsity_tolerance), N.ptr(mv), N.ptr(en),
+                                          N.ptr(nv), N.stream_handle()))
+    if int(nv.item()) == 0:
+        raise ValueError("all candidate windows fall outside the reference frame")
+    m = mv.cpu().tolist()
+    return (m[0], m[1]), float(en.item())
+
+
 def search_stage(cur, ref, block_origin, block_size: int, center, search_range: int, step: int,
                  config: FmeConfig):
     """Best candidate of one stage for one block (fme.py:271-291)."""
+    if not _integer_path(cur, ref, (block_size,)):
+        return _search_stage_f64(cur, ref, block_origin, block_size, center, search_range, step, config)
     bayer = _frame_kind_pair(cur, ref)
     scale = 2 if bayer else 1
     height, width = cur.height // scale, cur.width // scale
@@ -246,6 +334,8 @@ def _fields_from_device(levels, pair: int, block_sizes) -> list:
 
 def estimate_motion(cur, ref, config: FmeConfig = FmeConfig()) -> list:
     """Hierarchical ME; one MotionField per level (fme.py:324-392), on the GPU."""
+    if not _integer_path(cur, ref, config.block_sizes):
+        return _estimate_motion_f64(cur, ref, config)
     bayer = _frame_kind_pair(cur, ref)
     torch = N.require_cuda()
     ps = D.PlaneSet(np.stack([cur.data, ref.data]), bayer, config)

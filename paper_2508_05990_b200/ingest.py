@@ -74,9 +74,9 @@ def decode(payload, width: int, height: int, fmt: str, *, frames: int = 1, row_b
     if isinstance(payload, torch.Tensor):
         src = payload.reshape(-1)
     else:
-        src = torch.from_numpy(np.frombuffer(payload, dtype=np.uint8) if isinstance(payload, (bytes, bytearray,
-                                                                                           memoryview))
-                               else np.ascontiguousarray(payload).reshape(-1).view(np.uint8))
+        host = (np.frombuffer(payload, dtype=np.uint8) if isinstance(payload, (bytes, bytearray, memoryview))
+                else np.ascontiguousarray(payload).reshape(-1).view(np.uint8))
+        src = torch.from_numpy(host if host.flags.writeable else host.copy())
     if src.numel() < fb * (frames - 1) + rb * height:
         raise ValueError(f"payload of {src.numel()} bytes is shorter than {frames} frame(s) of {width}x{height} {fmt}")
     src_dev = src.to(dev, non_blocking=bool(src.is_pinned())) if src.device.type != "cuda" else src

@@ -145,27 +145,35 @@ class ClipSession:
 
     ``run(raw, key_labels)`` takes a (T, H, W) uint8/uint16 Bayer (or luma)
     clip in host memory, runs ME -> refine -> decide -> predict on the GPU and
-    returns ``(labels (T, Hl, Wl) uint8 ndarray, kinds, refs, triggers)``.
+    returns ``(labels, kinds, refs, triggers)`` where ``labels`` is a list of T
+    (Hl, Wl) uint8 arrays.
 
     ``key_labels`` is either
       * a callable / mapping frame -> LabelMap consulted exactly once per key
-        frame, in frame order, as ``run_sequence`` does (decisions are read back
-        first, then the key frames' labels are uploaded), or
+        frame, in frame order, as ``run_sequence`` does, or
       * a (T, Hl, Wl) uint8 tensor (pinned for full speed) holding a label map
         for every frame; only the key frames' maps are used (reference
-        semantics), and the upload overlaps motion estimation.
+        semantics).
+
+    Data movement follows the reference's semantics rather than shipping whole
+    label stacks: a key frame's output IS its input label map
+    (pipeline.py:116-121 appends the injected LabelMap), so it is returned as
+    that host array and never copied back; a key map is uploaded only when a
+    predicted frame references it; only predicted frames' labels come back.
 
     With the default "previous" reference policy the clip is processed in
-    ``chunks`` frame ranges on three streams: the H2D copy of chunk c+1
-    overlaps pack + ME of chunk c; refine and the AEM scan follow; the label
-    chain then runs per chunk with each chunk's D2H overlapping the next
-    chunk's gathers.  Results are identical to ``run_sequence`` (the chunking
-    only changes launch boundaries).  The returned label array is owned by the
-    session and overwritten by the next ``run``.
+    ``chunks`` frame ranges, software-pipelined by ``lag`` chunks on three
+    streams: the H2D of chunk c+lag's raw frames, pack, ME, refine and the AEM
+    scan are queued before the host reads chunk c's decisions (by then long
+    finished), so the GPU never waits for the host; chunk c's needed key maps
+    are then uploaded, its label chain runs and its predicted labels stream
+    back while later chunks compute.  Results are identical to ``run_sequence`` (chunking
+    only changes launch boundaries).  Returned arrays owned by the session are
+    overwritten by the next ``run``.
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True, chunks: int = 10):
+                 bayer: bool = True, chunks: int = 10, lag: int = 2):
         if config.refine_enabled and config.fme.block_sizes[-1] * (2 if bayer else 1) < CABR_MIN_BLOCK:
             raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                              f"{config.fme.block_sizes[-1] * (2 if bayer else 1)}-pixel blocks; disable refinement "
@@ -183,159 +191,158 @@ class ClipSession:
         k = max(1, min(int(chunks), t))
         bounds = [round(i * t / k) for i in range(k + 1)]
         self.chunks = [(bounds[i], bounds[i + 1]) for i in range(k) if bounds[i + 1] > bounds[i]]
+        self.lag = max(1, int(lag))
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
     # -- helpers ----------------------------------------------------------------
-    def _lookup_keys(self, lookup, kinds):
-        eng, torch = self.eng, self.torch
-        h2d = 0
-        for i in np.nonzero(kinds == 0)[0].tolist():
-            try:
-                lab = lookup(i)
-            except (KeyError, IndexError, FileNotFoundError):
-                raise MissingKeyLabels(i) from None
-            if lab is None:
-                raise MissingKeyLabels(i)
-            if (lab.height, lab.width) != (eng.Hl, eng.Wl):
-                raise ValueError("key label maps must match the session's label size")
-            np.copyto(self.pin_key[i].numpy(), lab.classes)
-            eng.key_labels[0, i].copy_(self.pin_key[i], non_blocking=True)
-            h2d += lab.classes.nbytes
-        return h2d
-
-    def _run_streamed(self, src, label_tensor, h2d):
-        """Fully chunked pass ("previous" policy, labels as a tensor): per frame chunk
-        H2D (raw + label maps) -> pack -> ME -> refine -> AEM scan (resumable state)
-        -> label chain -> D2H, so copies in both directions overlap the kernels of
-        neighbouring chunks.  Every step only needs frames of its own or earlier
-        chunks (pair t uses frames t-1, t; the AEM scan and the label chain are
-        causal), so results equal the whole-clip pass."""
+    def _motion_chunk(self, src, f0: int, f1: int) -> None:
+        """H2D of frames [f0, f1) (copy stream), then pack, ME of the pairs whose frames
+        are resident, refine and the AEM scan of those frames (compute stream)."""
         eng, torch = self.eng, self.torch
         lib = N.load()
         cs = torch.cuda.current_stream()
         st = N.stream_handle(cs)
         p = eng.params
-        fstride = p.frame_stride
-        esz = eng.planes.element_size()
-        cells2 = eng.gh * eng.gw * 2
-        fs = eng.Hl * eng.Wl
-        eng._reset_state()
-        self.copy_in.wait_stream(cs)  # previous users of the input buffers are done
-        for f0, f1 in self.chunks:
-            ev_in = torch.cuda.Event()
-            with torch.cuda.stream(self.copy_in):
-                eng.raw[0, f0:f1].copy_(src[f0:f1], non_blocking=True)
-                eng.key_labels[0, f0:f1].copy_(label_tensor[f0:f1], non_blocking=True)
-                ev_in.record(self.copy_in)
-            cs.wait_event(ev_in)
-            N.check(lib.bmc_pack_planes(N.ptr(eng.raw[0, f0]), f1 - f0, eng.kind_code, ctypes.byref(p),
-                                        N.ptr(eng.planes) + f0 * fstride * esz, st))
-            p0, p1 = max(f0, 1) - 1, f1 - 1
-            if p1 > p0:
-                arr = eng._level_slice(p0, p1)
-                N.check(lib.bmc_estimate_motion(N.ptr(eng.planes), eng.S * eng.T, ctypes.byref(p), p1 - p0,
-                                                N.ptr(eng.cur_index[p0:p1]), N.ptr(eng.ref_index[p0:p1]), arr, st))
-                eng._refine(p0, p1)
-                eng._decide(p0 + 1, p1 + 1)
-            eng._chain(f0, f1)
-            ev_out = torch.cuda.Event()
-            ev_out.record(cs)
-            with torch.cuda.stream(self.copy_out):
-                self.copy_out.wait_event(ev_out)
-                self.pin_labels[f0:f1].copy_(eng.labels[0, f0:f1], non_blocking=True)
-        dec = torch.stack([eng.kind[0].double(), eng.ref[0].double(), eng.trigger[0]])
         ev = torch.cuda.Event()
-        ev.record(cs)
+        with torch.cuda.stream(self.copy_in):
+            eng.raw[0, f0:f1].copy_(src[f0:f1], non_blocking=True)
+            ev.record(self.copy_in)
+        cs.wait_event(ev)
+        N.check(lib.bmc_pack_planes(N.ptr(eng.raw[0, f0]), f1 - f0, eng.kind_code, ctypes.byref(p),
+                                    N.ptr(eng.planes) + f0 * p.frame_stride * eng.planes.element_size(), st))
+        p0, p1 = max(f0, 1) - 1, f1 - 1  # pairs t in [max(f0,1), f1): both frames resident
+        if p1 > p0:
+            arr = eng._level_slice(p0, p1)
+            N.check(lib.bmc_estimate_motion(N.ptr(eng.planes), eng.S * eng.T, ctypes.byref(p), p1 - p0,
+                                            N.ptr(eng.cur_index[p0:p1]), N.ptr(eng.ref_index[p0:p1]), arr, st))
+            eng._refine(p0, p1)
+            eng._decide(p0 + 1, p1 + 1)
+
+    def _decisions_out(self, f0: int, f1: int):
+        """D2H of frames [f0, f1)'s decisions (copy-out stream, after the compute stream's AEM scan)."""
+        eng, torch = self.eng, self.torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
         with torch.cuda.stream(self.copy_out):
             self.copy_out.wait_event(ev)
-            self.pin_dec.copy_(dec, non_blocking=True)
-        self.copy_out.synchronize()
-        kinds = self.pin_dec[0].numpy().astype(np.int32)
-        refs = self.pin_dec[1].numpy().astype(np.int32)
-        trig = self.pin_dec[2].numpy().copy()
-        self.h2d_bytes = h2d + label_tensor.numel()
-        self.d2h_bytes = self.pin_dec.numel() * 8 + self.pin_labels.numel()
-        return self.pin_labels.numpy(), kinds, refs, trig
+            self.pin_dec[0, f0:f1].copy_(eng.kind[0, f0:f1], non_blocking=True)
+            self.pin_dec[1, f0:f1].copy_(eng.ref[0, f0:f1], non_blocking=True)
+            self.pin_dec[2, f0:f1].copy_(eng.trigger[0, f0:f1], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.copy_out)
+        return done
 
-    def run(self, raw, key_labels):
+    def _finish_chunk(self, f0: int, f1: int, dec_done, state) -> None:
+        """Host reads frames [f0, f1)'s decisions, consults the key labels, uploads the key
+        maps predicted frames reference, runs the chunk's label chain and streams the
+        predicted frames' labels back."""
         eng, torch = self.eng, self.torch
-        lib = N.load()
+        dec_done.synchronize()
+        kinds = self.pin_dec[0, f0:f1].numpy().astype(np.int32)
+        refs = self.pin_dec[1, f0:f1].numpy().astype(np.int32)
+        all_kinds = state["kinds"]
+        all_kinds[f0:f1] = kinds
+        for i in range(f0, f1):
+            if kinds[i - f0] == 0:
+                state["key_host"][i] = self._key_map(state, i)
+        need = sorted({int(r) for k, r in zip(kinds, refs) if k != 0 and all_kinds[int(r)] == 0}
+                      - state["uploaded"])
         cs = torch.cuda.current_stream()
-        st = N.stream_handle(cs)
-        src = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(raw))
-        if not src.is_pinned():
-            self.pin_raw.copy_(src)
-            src = self.pin_raw
-        label_tensor = key_labels if isinstance(key_labels, torch.Tensor) else None
-        lookup = None
-        if label_tensor is None:
-            lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
-        elif tuple(label_tensor.shape) != tuple(eng.labels.shape[1:]):
-            raise ValueError(f"key label tensor must be {tuple(eng.labels.shape[1:])}, got {tuple(label_tensor.shape)}")
-        h2d = src.numel() * src.element_size()
-        p = eng.params
-        fstride = p.frame_stride
-        esz = eng.planes.element_size()
-        eng._reset_state()
-        pipelined = eng.cfg.reference_policy == "previous" and eng.T >= 2
-        if pipelined and label_tensor is not None:
-            return self._run_streamed(src, label_tensor, h2d)
-        if pipelined:
-            for f0, f1 in self.chunks:
-                ev = torch.cuda.Event()
-                with torch.cuda.stream(self.copy_in):
-                    self.copy_in.wait_stream(cs)  # previous users of eng.raw are done
-                    eng.raw[0, f0:f1].copy_(src[f0:f1], non_blocking=True)
-                    ev.record(self.copy_in)
-                cs.wait_event(ev)
-                N.check(lib.bmc_pack_planes(N.ptr(eng.raw[0, f0]), f1 - f0, eng.kind_code, ctypes.byref(p),
-                                            N.ptr(eng.planes) + f0 * fstride * esz, st))
-                p0, p1 = max(f0, 1) - 1, f1 - 1  # pairs whose frames are resident: t in [max(f0,1), f1)
-                if p1 > p0:
-                    arr = eng._level_slice(p0, p1)
-                    N.check(lib.bmc_estimate_motion(N.ptr(eng.planes), eng.S * eng.T, ctypes.byref(p), p1 - p0,
-                                                    N.ptr(eng.cur_index[p0:p1]), N.ptr(eng.ref_index[p0:p1]), arr, st))
-            if label_tensor is not None:
-                ev_lab = torch.cuda.Event()
-                with torch.cuda.stream(self.copy_in):
-                    eng.key_labels[0].copy_(label_tensor, non_blocking=True)
-                    ev_lab.record(self.copy_in)
-            eng._refine(0, eng.n_pairs)
-            eng._decide(1, eng.T)
-        else:
-            eng.raw[0].copy_(src, non_blocking=True)
-            eng.motion()
-            if label_tensor is not None:
-                eng.key_labels[0].copy_(label_tensor, non_blocking=True)
-        dec = torch.stack([eng.kind[0].double(), eng.ref[0].double(), eng.trigger[0]])
-        d2h = self.pin_dec.numel() * 8  # kind, ref, trigger (float64 rows)
-        if label_tensor is None:
-            self.pin_dec.copy_(dec)  # synchronous: the key lookups need the decisions
-            kinds = self.pin_dec[0].numpy().astype(np.int32)
-            h2d += self._lookup_keys(lookup, kinds)
-        else:
-            if pipelined:
-                cs.wait_event(ev_lab)
-            h2d += label_tensor.numel()  # whole tensor uploaded (every frame's map is an input)
-        # label chain per chunk; each chunk's D2H overlaps the next chunk's gathers
-        cells2 = eng.gh * eng.gw * 2
-        fs = eng.Hl * eng.Wl
-        chunks = self.chunks if pipelined else [(0, eng.T)]
-        for f0, f1 in chunks:
-            eng._chain(f0, f1)
+        if need:
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(self.copy_in):
+                for r in need:
+                    # a key in this chunk goes to key_labels (its chain copies it into labels);
+                    # one in an earlier chunk was already chained, so it goes straight to labels
+                    dst = eng.key_labels[0, r] if r >= f0 else eng.labels[0, r]
+                    host = state["key_host"][r]
+                    if isinstance(host, torch.Tensor) and host.is_pinned():
+                        dst.copy_(host, non_blocking=True)
+                    else:
+                        self.pin_key[r].numpy()[...] = host
+                        dst.copy_(self.pin_key[r], non_blocking=True)
+                    state["h2d"] += eng.Hl * eng.Wl
+                ev.record(self.copy_in)
+            cs.wait_event(ev)
+            state["uploaded"].update(need)
+        eng._chain(f0, f1)
+        pred = [i for i in range(f0, f1) if kinds[i - f0] != 0]
+        if pred:
             ev = torch.cuda.Event()
             ev.record(cs)
             with torch.cuda.stream(self.copy_out):
                 self.copy_out.wait_event(ev)
-                self.pin_labels[f0:f1].copy_(eng.labels[0, f0:f1], non_blocking=True)
-        if label_tensor is not None:
-            with torch.cuda.stream(self.copy_out):
-                self.pin_dec.copy_(dec, non_blocking=True)
+                i = 0
+                while i < len(pred):  # runs of consecutive predicted frames, one copy each
+                    j = i
+                    while j + 1 < len(pred) and pred[j + 1] == pred[j] + 1:
+                        j += 1
+                    self.pin_labels[pred[i]:pred[j] + 1].copy_(eng.labels[0, pred[i]:pred[j] + 1], non_blocking=True)
+                    state["d2h"] += (pred[j] + 1 - pred[i]) * eng.Hl * eng.Wl
+                    i = j + 1
+
+    def _key_map(self, state, i: int):
+        """Key frame i's label map as a host array/tensor (the reference's lookup, in frame order)."""
+        eng = self.eng
+        tensor = state["tensor"]
+        if tensor is not None:
+            return tensor[i]
+        try:
+            lab = state["lookup"](i)
+        except (KeyError, IndexError, FileNotFoundError):
+            raise MissingKeyLabels(i) from None
+        if lab is None:
+            raise MissingKeyLabels(i)
+        if (lab.height, lab.width) != (eng.Hl, eng.Wl):
+            raise ValueError("key label maps must match the session's label size")
+        return lab.classes
+
+    def run(self, raw, key_labels):
+        eng, torch = self.eng, self.torch
+        src = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(raw))
+        if not src.is_pinned():
+            self.pin_raw.copy_(src)
+            src = self.pin_raw
+        tensor = key_labels if isinstance(key_labels, torch.Tensor) else None
+        if tensor is not None and tuple(tensor.shape) != tuple(eng.labels.shape[1:]):
+            raise ValueError(f"key label tensor must be {tuple(eng.labels.shape[1:])}, got {tuple(tensor.shape)}")
+        lookup = None
+        if tensor is None:
+            lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
+        state = {"tensor": tensor, "lookup": lookup, "kinds": np.full(eng.T, -1, np.int32), "key_host": {},
+                 "uploaded": set(), "h2d": src.numel() * src.element_size(), "d2h": 0}
+        self.copy_in.wait_stream(torch.cuda.current_stream())  # earlier users of the device buffers are done
+        eng._reset_state()
+        if eng.cfg.reference_policy == "previous" and eng.T >= 2:
+            pending = []
+            for f0, f1 in self.chunks:
+                self._motion_chunk(src, f0, f1)
+                pending.append((f0, f1, self._decisions_out(f0, f1)))
+                if len(pending) > self.lag:  # the GPU keeps `lag` chunks of motion work queued
+                    self._finish_chunk(*pending.pop(0), state)
+            for item in pending:
+                self._finish_chunk(*item, state)
+        else:  # "keyframe" policy (each ME's reference comes from the previous decision) or T == 1
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(self.copy_in):
+                eng.raw[0].copy_(src, non_blocking=True)
+                ev.record(self.copy_in)
+            torch.cuda.current_stream().wait_event(ev)
+            eng.motion()  # pack, reset, per-frame ME -> refine -> decide with device-chosen references
+            done = self._decisions_out(0, eng.T)
+            self._finish_chunk(0, eng.T, done, state)
         self.copy_out.synchronize()
+        state["d2h"] += self.pin_dec.numel() * 8
         kinds = self.pin_dec[0].numpy().astype(np.int32)
         refs = self.pin_dec[1].numpy().astype(np.int32)
         trig = self.pin_dec[2].numpy().copy()
-        d2h += self.pin_labels.numel()
-        self.h2d_bytes, self.d2h_bytes = h2d, d2h
-        return self.pin_labels.numpy(), kinds, refs, trig
+        labels = []
+        for i in range(eng.T):
+            if kinds[i] == 0:
+                h = state["key_host"][i]
+                labels.append(h.numpy() if isinstance(h, torch.Tensor) else np.asarray(h))
+            else:
+                labels.append(self.pin_labels[i].numpy())
+        self.h2d_bytes, self.d2h_bytes = state["h2d"], state["d2h"]
+        return labels, kinds, refs, trig

@@ -124,6 +124,44 @@ def scene_cut_clip(width: int, height: int, frames: int, cut_at: int, seed: int 
     return np.stack([a if t < cut_at else b for t in range(frames)])
 
 
+def gen_translating_scene(width: int, height: int, frames: int, velocity, seed: int = 0, square_size: int = 48,
+                          start=None, fg_class: int = 1):
+    """Textured luma square over a textured background with exact labels
+    (restates synth.py:44-85 so the SPEC acceptance sequences are identical)."""
+    vx, vy = int(velocity[0]), int(velocity[1])
+    if frames < 1:
+        raise ValueError("need at least one frame")
+    if square_size >= min(width, height):
+        raise ValueError("square must fit inside the frame")
+    sx0, sy0 = (width // 4, height // 4) if start is None else (int(start[0]), int(start[1]))
+    for t in (0, frames - 1):
+        x, y = sx0 + vx * t, sy0 + vy * t
+        if x < 0 or y < 0 or x + square_size > width or y + square_size > height:
+            raise ValueError(f"square leaves the frame at t={t}: origin ({x}, {y})")
+    background = value_noise(width, height, seed)
+    patch = (value_noise(square_size, square_size, seed + 1, cell=8) // 2 + 112).astype(np.uint8)
+    out_frames, out_labels = [], []
+    for t in range(frames):
+        x, y = sx0 + vx * t, sy0 + vy * t
+        pixels = background.copy()
+        pixels[y:y + square_size, x:x + square_size] = patch
+        classes = np.zeros((height, width), dtype=np.uint8)
+        classes[y:y + square_size, x:x + square_size] = fg_class
+        out_frames.append(Frame(width=width, height=height, data=pixels, kind=FrameKind.LUMA))
+        out_labels.append(LabelMap(width=width, height=height, classes=classes, num_classes=max(2, fg_class + 1)))
+    return out_frames, out_labels
+
+
+def gen_scene_cut(width: int, height: int, frames: int, cut_at: int, seed: int = 0) -> list:
+    """Two unrelated static luma scenes joined at ``cut_at`` (restates synth.py:88-104)."""
+    if frames < 1:
+        raise ValueError("need at least one frame")
+    scene_a = value_noise(width, height, seed)
+    scene_b = value_noise(width, height, seed + 1000003)
+    return [Frame(width=width, height=height, data=(scene_a if t < cut_at else scene_b).copy(), kind=FrameKind.LUMA)
+            for t in range(frames)]
+
+
 def frames_of(clip: np.ndarray, pattern: FrameKind = FrameKind.BAYER_RGGB) -> list:
     return [Frame(width=c.shape[1], height=c.shape[0], data=c, kind=pattern) for c in clip]
 

@@ -445,3 +445,73 @@ def test_multistream_engine_ring_vote(cuda, policy):
         got = eng.labels[s].cpu().numpy()
         for t in range(T):
             np.testing.assert_array_equal(got[t], olab[t])
+
+
+# ---------------------------------------------------------------------------
+# float64 plane stacks (fme.py:188-190) and geometry outside the integer kernels
+# ---------------------------------------------------------------------------
+
+F64_CASES = [
+    # (P, h, w, block_sizes, stages, value range)
+    (4, 72, 96, (16, 8), ((3, 2), (1, 1), (1, 1)), 1.0),
+    (3, 64, 48, (16,), ((4, 1), (0, 1), (2, 1)), 0.2),
+    (1, 50, 70, (32, 16, 8), ((2, 4), (1, 2), (1, 1)), 3.0),
+    (4, 40, 40, (8,), ((2, 1), (1, 1), (1, 1)), 1e-3),
+]
+
+
+@pytest.mark.parametrize("case", range(len(F64_CASES)))
+def test_estimate_motion_float_stacks(cuda, case):
+    from paper_2508_05990_b200 import fme, mv_refine
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    P, h, w, bs, stages, hi = F64_CASES[case]
+    rng = np.random.default_rng(100 + case)
+    cur = rng.random((P, h, w)) * hi
+    ref = np.roll(cur, (1, -2), axis=(1, 2)) + rng.random((P, h, w)) * hi * 0.05
+    if case == 3:  # quantised values -> many exact ties
+        cur, ref = np.round(cur * 3e3) / 3e3, np.round(ref * 3e3) / 3e3
+    cfg = FmeConfig(stages=tuple(SearchStage(*s) for s in stages), block_sizes=bs, lam=0.3,
+                    sparsity_tolerance=0.01 * hi if hi <= 1 else 0.03)
+    c2, r2 = (cur[0], ref[0]) if P == 1 else (cur, ref)  # a 2-D ndarray is a one-plane stack
+    got = fme.estimate_motion(c2, r2, cfg)
+    want = O.estimate_motion(cur, ref, ocfg(cfg))
+    assert_levels_equal(got, want)
+    r_got = mv_refine.refine_mvs(got[-1], 1, cur=c2, ref=r2, config=cfg)
+    r_want = O.refine_mvs(want[-1], 1, cur, ref, ocfg(cfg))
+    np.testing.assert_array_equal(r_got.mv, r_want.mv)
+    np.testing.assert_array_equal(r_got.energy.view(np.int64), r_want.energy.view(np.int64))
+
+
+def test_estimate_motion_block_128_frames(cuda):
+    """FmeConfig admits any power-of-two block >= 8 (fme.py:65-67); 128 goes through
+    the float64 kernel on device-normalised planes, bit-exact."""
+    from paper_2508_05990_b200 import fme, synth
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    clip = synth.bayer_pan_clip(600, 520, 2, (6, -4), seed=8)
+    fr = synth.frames_of(clip)
+    cfg = FmeConfig(stages=(SearchStage(2, 4), SearchStage(1, 2), SearchStage(1, 1)), block_sizes=(128, 64))
+    got = fme.estimate_motion(fr[1], fr[0], cfg)
+    want = O.estimate_motion(O.search_planes(clip[1], True), O.search_planes(clip[0], True), ocfg(cfg))
+    assert_levels_equal(got, want)
+
+
+@pytest.mark.parametrize("bsize", [5, 12, 3])
+def test_search_stage_any_block_size(cuda, bsize):
+    from paper_2508_05990_b200 import fme
+    from paper_2508_05990_b200.frame_io import Frame, FrameKind
+    cfg = _cfgs()["lam0"]
+    rng = np.random.default_rng(bsize)
+    a = rng.integers(0, 256, (40, 44)).astype(np.uint8)
+    b = np.roll(a, (2, 1), axis=(0, 1))
+    for cur, ref, planes_c, planes_r in (
+            (Frame(44, 40, a, FrameKind.LUMA), Frame(44, 40, b, FrameKind.LUMA),
+             O.search_planes(a, False), O.search_planes(b, False)),
+            (a / 7.0, b / 7.0, (a / 7.0)[None], (b / 7.0)[None])):
+        for origin, center in (((10, 9), (0, 0)), ((0, 0), (-1, 2)), ((44 - bsize, 40 - bsize), (3, 3))):
+            got = fme.search_stage(cur, ref, origin, bsize, center, 3, 1, cfg)
+            mv, e, _ = O.stage_candidates(planes_r, planes_c[:, origin[1]:origin[1] + bsize,
+                                                             origin[0]:origin[0] + bsize],
+                                          origin, bsize, center, 3, 1, cfg.lam, cfg.sparsity_tolerance)
+            assert got[0] == tuple(mv) and np.float64(got[1]).view(np.int64) == np.float64(e).view(np.int64)
+    with pytest.raises(ValueError, match="all candidate windows fall outside"):
+        fme.search_stage(a / 1.0, b / 1.0, (0, 0), bsize, (-30, -30), 1, 1, cfg)

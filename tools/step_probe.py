@@ -1,9 +1,11 @@
 """Device-time split of one C2 bench step: the three captured graphs (pack+reset | ME | refine+AEM+chain),
 bracketed by CUDA events, L2 flushed before each step as in bench.py."""
 import sys, statistics
-sys.path.insert(0, '.')
+sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
 import numpy as np, torch
 import bench
+import _variant
+_variant.use_variant_from_env()
 from paper_2508_05990_b200.engine import ClipEngine
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 c = bench.CONFIGS[name]
