@@ -543,8 +543,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
-    while (*((volatile unsigned*)ctr) < target) {
-    }
+    while (*((volatile unsigned*)ctr) < target) __nanosleep(20);  // back off: spinning steals issue slots
     __threadfence();
   }
   __syncthreads();
@@ -616,27 +615,29 @@ __device__ void chain_vote_group(const PredictArgs& a, const uint8_t* src, const
   const bool use[4] = {!(any_clean && ft), !(any_clean && fb), !(any_clean && fl), !(any_clean && fr)};
   uint32_t w[4] = {0, 0, 0, 0};
   const int n = min(16, a.W - x0);
-  for (int e = 0; e < n; ++e) {
+  // the 16 pixels are independent: fully unrolled so their vote chains interleave
+  const int dT = ly + 1, dB = k - ly;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
     const int lx = x0 + e - xb;
     const int cls[4] = {byte_of(top, e), byte_of(bot, e), left, right};
-    const int dist[4] = {ly + 1, k - ly, lx + 1, k - lx};
+    const int dist[4] = {dT, dB, lx + 1, k - lx};
     int dmin = 0x7fffffff;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
       if (use[c]) dmin = min(dmin, dist[c]);
-    int best = 0, best_votes = -1;
+    // key = (4 - votes) * 256 + class: the smallest key has the most votes, ties to the smallest class
+    int best_key = 0x7fffffff;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      if (!use[c] || dist[c] != dmin) continue;
+      const bool at = use[c] && dist[c] == dmin;
       int votes = 0;
 #pragma unroll
-      for (int c2 = 0; c2 < 4; ++c2) votes += use[c2] && dist[c2] == dmin && cls[c2] == cls[c];
-      if (votes > best_votes || (votes == best_votes && cls[c] < best)) {
-        best_votes = votes;
-        best = cls[c];
-      }
+      for (int c2 = 0; c2 < 4; ++c2) votes += (use[c2] && dist[c2] == dmin && cls[c2] == cls[c]) ? 1 : 0;
+      const int key = (4 - votes) * 256 + cls[c];
+      best_key = at ? min(best_key, key) : best_key;
     }
-    w[e >> 2] |= (uint32_t)best << (8 * (e & 3));
+    w[e >> 2] |= (uint32_t)(best_key & 0xff) << (8 * (e & 3));
   }
   if (vec_ok && n == 16) {
     *reinterpret_cast<uint4*>(out_row + x0) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -645,10 +646,47 @@ __device__ void chain_vote_group(const PredictArgs& a, const uint8_t* src, const
   }
 }
 
+// The same vote for ONE pixel (y, x) of a flagged block: the chain spreads a
+// frame's flagged pixels over the whole grid (one pixel per thread) instead of
+// giving one thread 16 of them.
+__device__ __forceinline__ void chain_vote_pixel(const PredictArgs& a, const uint8_t* src, const int32_t* mv,
+                                                 const uint8_t* m, uint8_t* out, int y, int x, int lb) {
+  const int k = a.B;  // a power of two here (k == 1 << lb)
+  const int y0 = (y >> lb) << lb, xb = (x >> lb) << lb, ly = y - y0, lx = x - xb;
+  const int ty = min(max(y0 - 1, 0), a.H - 1), by = min(max(y0 + k, 0), a.H - 1);
+  const int lxp = min(max(xb - 1, 0), a.W - 1), rxp = min(max(xb + k, 0), a.W - 1);
+  const int ry[4] = {ty, by, y, y}, rx[4] = {x, x, lxp, rxp};
+  const int dist[4] = {ly + 1, k - ly, lx + 1, k - lx};
+  int cls[4];
+  bool fl[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {  // the four ring pixels' unrefined predictions: independent load chains
+    const int cell = (ry[c] >> lb) * a.gw + (rx[c] >> lb);
+    const int dx = __ldg(mv + 2 * cell) * a.scale, dy = __ldg(mv + 2 * cell + 1) * a.scale;
+    cls[c] = __ldcg(src + (long long)min(max(ry[c] + dy, 0), a.H - 1) * a.W + min(max(rx[c] + dx, 0), a.W - 1));
+    fl[c] = m[cell] == 0;
+  }
+  const bool any_clean = !(fl[0] && fl[1] && fl[2] && fl[3]);
+  int dmin = 0x7fffffff;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (!(any_clean && fl[c])) dmin = min(dmin, dist[c]);
+  int best_key = 0x7fffffff;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const bool at = !(any_clean && fl[c]) && dist[c] == dmin;
+    int votes = 0;
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) votes += (!(any_clean && fl[c2]) && dist[c2] == dmin && cls[c2] == cls[c]) ? 1 : 0;
+    best_key = at ? min(best_key, (4 - votes) * 256 + cls[c]) : best_key;
+  }
+  out[(long long)y * a.W + x] = (uint8_t)(best_key & 0xff);
+}
+
 // Gather of one 16-pixel group of a non-key frame t of one stream
 // (propagate.py:39-53): out[y, x] = ref[clip(y + s*dy), clip(x + s*dx)].
 __device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int stream, int t, long long o, int y, int x0,
-                                                   bool vec_ok) {
+                                                   bool vec_ok, bool skip_flagged = false) {
   uint8_t* out = a.labels + stream * a.ss + t * a.fs + (long long)y * a.W;
   const int n = min(16, a.W - x0);
   const int r = a.ref ? a.ref[o] : a.ref_fixed;
@@ -657,7 +695,7 @@ __device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int str
   if (a.matched) {  // CaBR ring vote on flagged blocks (cells indexed like mv, one byte per cell)
     const uint8_t* m = a.matched + stream * (a.mvss / 2) + t * (a.mvfs / 2);
     if (m[(y / a.B) * a.gw + x0 / a.B] == 0) {
-      chain_vote_group(a, src, mv, m, out, y, x0, vec_ok);
+      if (!skip_flagged) chain_vote_group(a, src, mv, m, out, y, x0, vec_ok);
       return;
     }
   }
@@ -714,9 +752,14 @@ __device__ __forceinline__ void chain_gather_group(const PredictArgs& a, int str
 // predicted frame is ONE pass: plain gathers, and on flagged blocks (ring vote
 // enabled) the fused predict + vote of chain_vote_group.
 constexpr int kChainKindsSmem = 2048;
+constexpr int kChainScanCells = 8192;  // cells (all streams) a CTA scans per frame for the flagged list
+constexpr int kChainFlagCap = 2048;    // flagged blocks per frame handled per pixel
 __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictArgs a, int n_streams, int t_begin,
                                                                  int t_end, unsigned* barrier_ctr) {
   __shared__ int kind_s[kChainKindsSmem];
+  __shared__ int flag_list[kChainFlagCap];
+  __shared__ int flag_n;
+  __shared__ int warp_tot[kThreads / 32];
   const int groups_per_row = (a.W + 15) / 16;
   const long long per_stream = (long long)a.H * groups_per_row;
   const long long total = per_stream * n_streams;
@@ -777,19 +820,92 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
   }
   unsigned epoch = 0;
   if (a.kind) grid_barrier(barrier_ctr, ++epoch * gridDim.x);  // key frames visible to the gathers
-  // ---- phase 2: non-key frames in order
+  // ---- phase 2: non-key frames in order.  A thread's (stream, row, group) tasks
+  // are the same for every frame: decode them once (32-bit, no 64-bit divides in
+  // the frame loop); threads with more than kTasks tasks decode the rest per frame.
+  constexpr int kTasks = 4;
+  int ts[kTasks], ty[kTasks], tx[kTasks];
+  int ntask = 0;
+  const uint32_t gpr = (uint32_t)groups_per_row, pss = (uint32_t)per_stream;
+  for (long long g = gtid; g < total && ntask < kTasks; g += stride, ++ntask) {
+    const uint32_t gg32 = (uint32_t)g;
+    ts[ntask] = (int)(gg32 / pss);
+    const uint32_t rem = gg32 - (uint32_t)ts[ntask] * pss;
+    ty[ntask] = (int)(rem / gpr);
+    tx[ntask] = (int)(rem - (uint32_t)ty[ntask] * gpr) * 16;
+  }
+  const long long g_rest = gtid + (long long)kTasks * stride;
+  // Ring vote per pixel: every CTA lists the frame's flagged blocks (all
+  // streams) in shared memory, then the grid takes one flagged pixel per thread
+  // -- instead of one thread voting 16 pixels while its warp waits.  Only when
+  // the cells of a frame fit the scan budget and the list fits (else per group).
+  const int cells = a.gh * a.gw;
+  const bool pix_vote = a.matched && (long long)n_streams * cells <= kChainScanCells &&
+                        (a.B & (a.B - 1)) == 0 && (long long)kChainFlagCap * a.B * a.B < (1ll << 31);
   bool prev_wrote = false;
   for (int t = t_begin; t < t_end; ++t) {
     const bool work = !a.kind || frame_has(t, false);
     if (!work) continue;
     // frame t reads frames <= t-1: any phase-2 work since the last barrier needs one first
     if (prev_wrote) grid_barrier(barrier_ctr, ++epoch * gridDim.x);
-    for (long long g = gtid; g < total; g += stride) {
-      const int stream = (int)(g / per_stream);
+    bool per_pixel = false;
+    if (pix_vote) {
+      // ordered compaction (identical list in every CTA): thread i owns cells
+      // [i*chunk, (i+1)*chunk), exclusive scan of the per-thread counts
+      const int ncell = n_streams * cells;
+      const int chunk = (ncell + blockDim.x - 1) / blockDim.x;
+      const int c0 = threadIdx.x * chunk, c1 = min(ncell, c0 + chunk);
+      auto is_flagged = [&](int i) {
+        const int st = i / cells, c = i - st * cells;
+        return kind_of(st, t) != 0 && a.matched[st * (a.mvss / 2) + t * (a.mvfs / 2) + c] == 0;
+      };
+      int cnt = 0;
+      for (int i = c0; i < c1; ++i) cnt += is_flagged(i);
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      int incl = cnt;
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      if (lane == 31) warp_tot[wid] = incl;
+      __syncthreads();
+      int base = 0;
+      for (int w = 0; w < wid; ++w) base += warp_tot[w];
+      if (threadIdx.x == blockDim.x - 1) flag_n = base + incl;
+      int slot = base + incl - cnt;
+      for (int i = c0; i < c1; ++i)
+        if (is_flagged(i)) {
+          if (slot < kChainFlagCap) flag_list[slot] = i;
+          ++slot;
+        }
+      __syncthreads();
+      per_pixel = flag_n <= kChainFlagCap;  // the same in every CTA
+    }
+#pragma unroll
+    for (int q = 0; q < kTasks; ++q) {
+      if (q < ntask && kind_of(ts[q], t) != 0)
+        chain_gather_group(a, ts[q], t, (long long)ts[q] * a.kss + t, ty[q], tx[q], vec_ok, per_pixel);
+    }
+    for (long long g = g_rest; g < total; g += stride) {
+      const uint32_t gg32 = (uint32_t)g;
+      const int stream = (int)(gg32 / pss);
       if (kind_of(stream, t) == 0) continue;
-      const long long gg = g - stream * per_stream;
-      const int y = (int)(gg / groups_per_row), x0 = (int)(gg - (long long)y * groups_per_row) * 16;
-      chain_gather_group(a, stream, t, (long long)stream * a.kss + t, y, x0, vec_ok);
+      const uint32_t rem = gg32 - (uint32_t)stream * pss;
+      const int y = (int)(rem / gpr), x0 = (int)(rem - (uint32_t)y * gpr) * 16;
+      chain_gather_group(a, stream, t, (long long)stream * a.kss + t, y, x0, vec_ok, per_pixel);
+    }
+    if (per_pixel) {
+      const int lb = __ffs(a.B) - 1, lkk = 2 * lb;
+      const int npix = flag_n << lkk;  // <= kChainFlagCap * B^2
+      for (int q = (int)gtid; q < npix; q += (int)stride) {
+        const int id = flag_list[q >> lkk], pix = q & ((1 << lkk) - 1);
+        const int st = id / cells, c = id - st * cells;
+        const int y = (c / a.gw) * a.B + (pix >> lb), x = (c % a.gw) * a.B + (pix & (a.B - 1));
+        if (y >= a.H || x >= a.W) continue;
+        const uint8_t* src = a.labels + st * a.ss + (long long)a.ref[(long long)st * a.kss + t] * a.fs;
+        chain_vote_pixel(a, src, a.mv + st * a.mvss + t * a.mvfs, a.matched + st * (a.mvss / 2) + t * (a.mvfs / 2),
+                         a.labels + st * a.ss + t * a.fs, y, x, lb);
+      }
     }
     prev_wrote = true;
   }
@@ -807,6 +923,10 @@ int launch_predict_chain(const PredictArgs& a, int n_streams, int t_begin, int t
     if (per_sm < 1) per_sm = 1;
   }
   const long long tasks = (long long)n_streams * a.H * ((a.W + 15) / 16);
+  if (tasks >= (1ll << 31)) {
+    set_error("label chain of %lld 16-pixel groups exceeds the kernel's 32-bit task index", tasks);
+    return BMC_E_ARG;
+  }
   long long grid = (tasks + kThreads - 1) / kThreads;
   int use_per_sm = per_sm;
   if (const char* v = knob_env("BMC_CHAIN_PER_SM")) use_per_sm = std::max(1, std::min(per_sm, atoi(v)));
