@@ -78,6 +78,65 @@ int bmc_confusion(const uint8_t* pred, const uint8_t* truth, int64_t n, int n_ma
                   int num_classes, int ignore_class, unsigned long long* confusion, int32_t* overflow,
                   void* stream);
 
+/* ------------------------------------------------------------------ CaBR --
+ * CaBR-Net forward pass (cabr.py:206-250) on device, fp32 (the reference's
+ * float32 einsum; results agree within fp32 rounding, not bit for bit).
+ * Weights: `payload` is the reference's weight payload -- every tensor of
+ * weight_spec(num_classes) (cabr.py:97-119) in order, float32, concatenated
+ * (exactly the bytes after the JSON header of save_weights, cabr.py:152-168),
+ * already in device memory; bmc_cabr_pack_weights re-lays it out for the
+ * kernel into `packed` (bmc_cabr_weight_floats(num_classes) floats).
+ * num_classes <= 256 (uint8 labels); block sizes K >= 16, multiples of 16.
+ *
+ * bmc_cabr_forward_blocks: cabr_forward(extract_patch(frame, labels, origin, K))
+ *   (cabr.py:60-90) for n_blocks origins (int32 (x, y) pairs) of ONE frame:
+ *   pixels (height, width) uint8 (pixel_kind 0) / uint16 (1), divided by the
+ *   dtype maximum, or float32 used as-is (2); labels (height, width) uint8.
+ *   logits_out (n, C, K, K) float32 and/or argmax_out (n, K, K) uint8 (first
+ *   maximum, np.argmax), either may be NULL.
+ * bmc_cabr_forward_patches: cabr_forward on explicit CabrPatch tensors, image
+ *   (n, 1, S, S) and context (n, C, S, S) float32, S = 2K+1 (any context values).
+ * bmc_cabr_chain: the label chain of frames [t_begin, t_end) with the network
+ *   refining every flagged block of every predicted frame, as run_sequence does
+ *   with weights (pipeline.py:123-135, refine_blocks cabr.py:306-345): per
+ *   frame, plain prediction (bmc_predict_labels), the forward pass over the
+ *   frame's flagged blocks (final-level matched == 0, all streams), then the
+ *   write-back; the refined labels feed later frames.  Arguments as
+ *   bmc_predict_labels_clip, plus the raw frames (pixels, uint8/uint16, frame t
+ *   of stream s at + s*pix_stream_stride + t*pix_frame_stride elements; same
+ *   size as the labels), the packed weights, scratch ((n_streams, H, W) bytes)
+ *   and workspace (bmc_cabr_chain_workspace bytes). */
+size_t bmc_cabr_weight_floats(int num_classes);
+int bmc_cabr_pack_weights(const float* payload, int num_classes, float* packed, void* stream);
+int bmc_cabr_forward_blocks(const void* pixels, int pixel_kind, const uint8_t* labels, int height, int width,
+                            const int32_t* origins, int n_blocks, int block_size, int num_classes,
+                            const float* packed, float* logits_out, uint8_t* argmax_out, void* stream);
+int bmc_cabr_forward_patches(const float* image, const float* context, int n_patches, int block_size,
+                             int num_classes, const float* packed, float* logits_out, uint8_t* argmax_out,
+                             void* stream);
+/* extract_patch (cabr.py:60-90) for n origins of one frame: image_out
+ * (n, 1, S, S) float32, context_out (n, C, S, S) float32 (masked one-hot). */
+int bmc_cabr_extract_patches(const void* pixels, int pixel_kind, const uint8_t* labels, int height, int width,
+                             const int32_t* origins, int n, int block_size, int num_classes, float* image_out,
+                             float* context_out, void* stream);
+/* refine_blocks (cabr.py:306-345) on one frame: labels_out = labels_in with
+ * every listed block (origins (n, 2) int32 (x, y), >= 0) re-labelled from
+ * labels_in -- by the network's argmax when `packed` is given, else by the
+ * weight-free ring vote (_ring_vote, cabr.py:257-303) -- written back clipped
+ * to the frame in list order.  staging: n*K*K bytes; owner: H*W int32;
+ * flagged: H*W bytes (ring vote only, may be NULL with weights). */
+int bmc_refine_blocks(const void* pixels, int pixel_kind, const uint8_t* labels_in, uint8_t* labels_out,
+                      int height, int width, const int32_t* origins, int n, int block_size, int num_classes,
+                      const float* packed, uint8_t* staging, int32_t* owner, uint8_t* flagged, void* stream);
+size_t bmc_cabr_chain_workspace(int n_streams, int n_frames, int grid_h, int grid_w);
+int bmc_cabr_chain(uint8_t* labels, int64_t frame_stride, int64_t stream_stride, const uint8_t* key_labels,
+                   int n_streams, int t_begin, int t_end, const int32_t* kind, const int32_t* ref,
+                   int64_t kind_stream_stride, int height, int width, const int32_t* mv, int64_t mv_frame_stride,
+                   int64_t mv_stream_stride, int grid_h, int grid_w, int block_size, int scale,
+                   const uint8_t* matched, const void* pixels, int pixel_kind, int64_t pix_frame_stride,
+                   int64_t pix_stream_stride, int num_classes, const float* packed, uint8_t* scratch,
+                   int32_t* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,21 @@ _SIGNATURES = {
                                       ctypes.c_int, vp, vp]),
     "bmc_pack_be16": (ctypes.c_int, [vp, i64, vp, vp]),
     "bmc_confusion": (ctypes.c_int, [vp, vp, i64, ctypes.c_int, i64, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
+    # CaBR-Net (include/bmc_ext.h)
+    "bmc_cabr_weight_floats": (ctypes.c_size_t, [ctypes.c_int]),
+    "bmc_cabr_pack_weights": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
+    "bmc_cabr_forward_blocks": (ctypes.c_int, [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
+    "bmc_cabr_forward_patches": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
+    "bmc_cabr_extract_patches": (ctypes.c_int, [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int, vp, vp, vp]),
+    "bmc_refine_blocks": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp]),
+    "bmc_cabr_chain_workspace": (ctypes.c_size_t, [ctypes.c_int] * 4),
+    "bmc_cabr_chain": (ctypes.c_int, [vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, i64,
+                                      ctypes.c_int, ctypes.c_int, vp, i64, i64, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int, i64, i64, ctypes.c_int, vp,
+                                      vp, vp, vp]),
 }
 
 RAW_BE16, RAW_MIPI10, RAW_MIPI12 = 0, 1, 2

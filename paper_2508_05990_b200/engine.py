@@ -112,6 +112,22 @@ class ClipEngine:
         self.key_labels = self.torch.zeros_like(self.labels)
         # CaBR weight-free fallback (ring vote) runs inside the label chain when refinement is on
         self.ring_vote = bool(self.cfg.refine_enabled)
+        self.cabr = None
+        self.graph = None
+
+    def set_cabr(self, weights) -> None:
+        """Refine flagged blocks with the CaBR-Net forward pass (cabr.py:306-345, weights given)
+        instead of the ring vote: the label chain becomes bmc_cabr_chain."""
+        from .cabr import packed_weights
+        if not self.cfg.refine_enabled:
+            raise ValueError("CaBR weights need refine_enabled")
+        if (self.Hl, self.Wl) != (self.H, self.W):
+            raise ValueError("frame and label map dimensions differ")
+        torch, lib = self.torch, N.load()
+        ws = lib.bmc_cabr_chain_workspace(self.S, self.T, self.gh, self.gw)
+        self.cabr = dict(packed=packed_weights(weights, torch, self.dev), C=weights.num_classes,
+                         scratch=torch.empty((self.S, self.Hl, self.Wl), dtype=torch.uint8, device=self.dev),
+                         workspace=torch.empty((ws + 3) // 4, dtype=torch.int32, device=self.dev))
         self.graph = None
 
     def load_frames(self, frames, non_blocking: bool = False) -> None:
@@ -202,10 +218,21 @@ class ClipEngine:
 
     def _chain(self, t0: int, t1: int) -> None:
         """Label chain of frames [t0, t1) of every stream (one cooperative launch); with
-        refine_enabled the flagged blocks of predicted frames get CaBR's ring vote."""
+        refine_enabled the flagged blocks of predicted frames get CaBR's ring vote, or
+        the network (set_cabr) frame by frame."""
         cells = self.gh * self.gw
         cells2 = cells * 2
         fs = self.Hl * self.Wl
+        if self.cabr is not None:
+            c = self.cabr
+            N.check(N.load().bmc_cabr_chain(
+                N.ptr(self.labels), fs, self.T * fs, N.ptr(self.key_labels), self.S, t0, t1, N.ptr(self.kind),
+                N.ptr(self.ref), self.T, self.Hl, self.Wl, N.ptr(self.mv_ref) - 4 * self.S * cells2,
+                self.S * cells2, cells2, self.gh, self.gw, self.b_final, self.scale,
+                N.ptr(self.levels[-1].matched) - self.S * cells, N.ptr(self.raw),
+                0 if self.raw.dtype == self.torch.uint8 else 1, self.H * self.W, self.T * self.H * self.W, c["C"],
+                N.ptr(c["packed"]), N.ptr(c["scratch"]), N.ptr(c["workspace"]), N.stream_handle()))
+            return
         ring = self.ring_vote
         matched = (N.ptr(self.levels[-1].matched) - self.S * cells) if ring else None
         N.check(N.load().bmc_predict_labels_clip(

@@ -228,7 +228,10 @@ def _device_planes(x, torch, dev):
         planes = torch.stack([t[k >> 1::2, k & 1::2] for k in range(4)])
     else:
         planes = t[None]
-    return planes.to(torch.float64) / float(x.max_value)
+    # a CUDA-tensor divisor: torch turns division by a Python scalar into a multiply
+    # by its reciprocal, which is not numpy's correctly rounded quotient
+    s = torch.tensor(float(x.max_value), dtype=torch.float64, device=dev)
+    return planes.to(torch.float64) / s
 
 
 def _pad_edge_device(planes, multiple: int, torch):

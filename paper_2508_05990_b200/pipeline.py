@@ -13,9 +13,9 @@ Semantics (decisions, labels, ledger) are identical to the reference's.  With
 ``refine_enabled`` (the default) and no CaBR weights the reference re-labels the
 flagged blocks of every predicted frame with its weight-free ring vote
 (cabr.py:257-345) and the refined labels feed later predictions; the label-chain
-kernel does the same on device.  Running the CaBR-Net forward pass itself
-(``weights`` given) is the next component on the roadmap and raises instead of
-silently skipping it.
+kernel does the same on device.  With ``weights`` the CaBR-Net forward pass
+re-labels them instead (``bmc_cabr_chain``: per predicted frame, prediction,
+the network over the frame's flagged blocks, write-back).
 """
 
 from __future__ import annotations
@@ -27,6 +27,7 @@ import numpy as np
 
 from . import _native as N
 from .config import PipelineConfig
+from .cabr import count_cabr_flops
 from .engine import ClipEngine
 from .fme import count_fme_flops, mv_scale
 from .frame_io import Frame, LabelMap
@@ -83,9 +84,6 @@ def run_sequence(frames, key_labels, config: PipelineConfig = PipelineConfig(), 
     if config.refine_enabled and final_block < CABR_MIN_BLOCK:
         raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                          f"{final_block}-pixel blocks; disable refinement or use larger blocks")
-    if config.refine_enabled and weights is not None:
-        raise NotImplementedError("the CaBR-Net forward pass (weights given) is not part of the B200 hot path yet; "
-                                  "pass weights=None for the ring-vote fallback or disable refinement")
     _check_clip(frames)
     planes = 4 if scale == 2 else 1
     backbone = round(config.backbone_gflops * 1e9)
@@ -113,6 +111,18 @@ def run_sequence(frames, key_labels, config: PipelineConfig = PipelineConfig(), 
             raise ValueError("all key label maps of a clip must share one size")
         injected[i] = lab
         eng.key_labels[0, i].copy_(eng.torch.from_numpy(np.array(lab.classes)))
+    use_net = config.refine_enabled and weights is not None
+    flagged = np.zeros(len(frames), dtype=np.int64)  # refinement_blocks per predicted frame
+    if use_net and len(frames) > 1:
+        m = eng.levels[-1].matched[:eng.n_pairs].cpu().numpy()
+        for i in range(1, len(frames)):
+            if kinds[i] != 0:
+                flagged[i] = int((m[eng.pair_index(0, i)] == 0).sum())
+    if use_net and flagged.any():
+        C = next(iter(injected.values())).num_classes
+        if weights.num_classes != C:
+            raise ValueError("weights and label map disagree on num_classes")
+        eng.set_cabr(weights)
     eng.predict()
     out = eng.labels[0].cpu().numpy()
 
@@ -135,6 +145,8 @@ def run_sequence(frames, key_labels, config: PipelineConfig = PipelineConfig(), 
             ref = int(refs[i])
             lab = LabelMap(width=eng.Wl, height=eng.Hl, classes=out[i], num_classes=labels[ref].num_classes)
             ledger.add("prediction", 0)
+            if use_net:
+                ledger.add("cabr", count_cabr_flops(eng.b_final * scale, labels[ref].num_classes, int(flagged[i])))
             decisions.append(FrameDecision(i, kind_from_code(kinds[i]), ref, float(trig[i])))
         labels.append(lab)
     return RunResult(labels=labels, decisions=decisions, ledger=ledger, scale=scale)
