@@ -60,12 +60,19 @@ CONFIGS = {
     "c5": (1920, 1080, 40, "c5", 7, ((4, 8), (2, 4), (2, 1)), (64, 32), "uint8",
            "1080p RGGB uint8 40-frame high-motion sweep + moving square + scene cut, standard preset (64->32 "
            "split), max_gop=5", {"max_gop": 5, "aem_threshold": float("inf"), "refine_enabled": False}),
+    # C5 with CaBR-Net re-inference of every flagged block of the predicted frames (refine_enabled, seeded
+    # random_weights(19, 0): the reference's run_sequence(..., weights) path, pipeline.py:127-135)
+    "c5cabr": (1920, 1080, 40, "c5", 7, ((4, 8), (2, 4), (2, 1)), (64, 32), "uint8",
+               "C5 clip with CaBR-Net (19 classes, seeded weights) re-labelling every flagged block of the 32 "
+               "predicted frames", {"max_gop": 5, "aem_threshold": float("inf"), "refine_enabled": True}),
     # C4: 64 independent C2 streams, stream k -> rank k mod N; seed 1000+k, SURVEY §8d velocities
     "c4": (1920, 1080, 30, None, 1000, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
            "64 streams of 1920x1080 RGGB uint8 30-frame clips, 16x16 blocks, +-16 full search, sharded across GPUs",
            {}),
 }
 C4_STREAMS = 64
+CABR_CLASSES = {"c5cabr": 19}  # configs that run the CaBR-Net (num_classes of the seeded weights)
+FFMA_LANES_PER_CLK_SM = 128.0  # fp32 FFMA issue rate (tools/sad_peak.cu ffma_f32, profiles/r02_sad_peak.jsonl)
 
 
 def c4_velocity(k):
@@ -279,6 +286,11 @@ def measure(name, args, rank, world, local_rank, stream_ids, flush):
     eng.load_frames(np.stack([cl for cl, _ in clips]))
     for k, (_c, labs) in enumerate(clips):
         eng.key_labels[k].copy_(torch.from_numpy(np.stack([labs[t].classes for t in range(T)])))
+    weights = None
+    if name in CABR_CLASSES:
+        from paper_2508_05990_b200 import cabr
+        weights = cabr.random_weights(CABR_CLASSES[name], seed=0)
+        eng.set_cabr(weights)
     eng.capture()
 
     def flush_l2():
@@ -315,7 +327,7 @@ def measure(name, args, rank, world, local_rank, stream_ids, flush):
     keyframes = int((kinds == 0).sum())
 
     # --- e2e through the public host-buffer API, every stream of this rank ---
-    sess = ClipSession(pcfg, H, W, T, dt, True)
+    sess = ClipSession(pcfg, H, W, T, dt, True, weights=weights)
     host_in = [(torch.from_numpy(cl).pin_memory(),
                 torch.from_numpy(np.stack([labs[t].classes for t in range(T)])).pin_memory()) for cl, labs in clips]
     for _ in range(2):
@@ -336,7 +348,14 @@ def measure(name, args, rank, world, local_rank, stream_ids, flush):
             d2h += sess.d2h_bytes
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
     e2e_ok = bool(np.array_equal(np.stack(out_labels), eng.labels[S - 1].cpu().numpy()))
-    return {"eng": eng, "pcfg": pcfg, "S": S, "W": W, "H": H, "T": T, "bpp": bpp, "step_ms": step_ms,
+    flagged = 0
+    if weights is not None:
+        mt = eng.levels[-1].matched[:eng.n_pairs].cpu().numpy()
+        for s_ in range(S):
+            for t in range(1, T):
+                if kinds[s_, t] != 0:
+                    flagged += int((mt[eng.pair_index(s_, t)] == 0).sum())
+    return {"name": name, "eng": eng, "pcfg": pcfg, "S": S, "flagged": flagged, "weights": weights, "W": W, "H": H, "T": T, "bpp": bpp, "step_ms": step_ms,
             "me_ms": me_ms, "post_ms": post_ms, "samples": samples, "predicted": predicted, "keyframes": keyframes,
             "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "e2e_ok": e2e_ok, "clocks": clocks.summary(), "dev": dev}
 
@@ -448,6 +467,12 @@ def run_b200(args, rank, world, local_rank):
             "compensation": _compensation_block(mv, p_ms, hbm_peak),
             "e2e": {"value": fr / (e_ms / 1e3), "unit": "frames/s", "h2d_bytes_per_step": mv["h2d"],
                     "d2h_bytes_per_step": mv["d2h"], "ms_per_step": e_ms, "labels_match_device_run": mv["e2e_ok"]}}
+    if name == "c5" and not args.no_variant:
+        # the same clip with the CaBR-Net re-labelling every flagged block of the predicted frames
+        del m, eng
+        torch.cuda.empty_cache()
+        mv = measure("c5cabr", args, rank, world, local_rank, stream_ids, flush)
+        line["variant_cabr"] = _cabr_block(mv, world, args, dev, sms)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
         try:
@@ -459,6 +484,36 @@ def run_b200(args, rank, world, local_rank):
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def _cabr_block(mv, world, args, dev, sms):
+    """Bench sub-line of a CaBR config: throughput, e2e, and the fp32 roofline of the network
+    (executed FLOPs of the receptive-field-cropped kernel per flagged block x blocks / the
+    post-ME time, which also holds refine + AEM + prediction, so the fraction is a lower bound)."""
+    from paper_2508_05990_b200 import cabr
+    t_ms, e_ms, p_ms, me_ms = _reduce_max([statistics.mean(mv["step_ms"]), statistics.mean(mv["e2e_ms"]),
+                                           statistics.mean(mv["post_ms"]), statistics.mean(mv["me_ms"])],
+                                          args, dev, world)
+    fr = (mv["T"] - 1) * mv["S"] * world
+    K = mv["eng"].b_final * mv["eng"].scale
+    C = mv["weights"].num_classes
+    ex = cabr.executed_flops(K, C) * mv["flagged"]
+    ref = cabr.count_cabr_flops(K, C, mv["flagged"])
+    clk = mv["clocks"].get("sm_mhz") or 1965.0
+    peak = FFMA_LANES_PER_CLK_SM * 2 * sms * clk * 1e6 / 1e12
+    achieved = ex / (p_ms / 1e3) / 1e12
+    return {"workload": CONFIGS[mv["name"]][8], "value": fr / (t_ms / 1e3), "unit": "frames/s", "ms_per_step": t_ms,
+            "me_ms": me_ms, "post_me_ms": p_ms, "predicted_frames_per_clip": mv["predicted"] // mv["S"],
+            "flagged_blocks_per_clip": mv["flagged"] // mv["S"], "block_px": K, "classes": C,
+            "roofline": {"bound": "fp32_ffma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "executed_gflop_per_clip": ex / 1e9 / mv["S"],
+                         "reference_layer_gflop_per_clip": ref / 1e9 / mv["S"],
+                         "peak_basis": f"{FFMA_LANES_PER_CLK_SM:.0f} FFMA/clk/SM x 2 x {sms} SMs x {clk:.0f} MHz",
+                         "kernel": "cabr_kernel (+ predict_kernel, cabr_scatter_kernel per frame) inside the "
+                                   "post-ME graph; time = events from the end of ME to the end of the step"},
+            "e2e": {"value": fr / (e_ms / 1e3), "unit": "frames/s", "h2d_bytes_per_step": mv["h2d"],
+                    "d2h_bytes_per_step": mv["d2h"], "ms_per_step": e_ms, "labels_match_device_run": mv["e2e_ok"]},
+            "clocks": mv["clocks"]}
 
 
 def _compensation_block(m, post_ms, hbm_peak):
@@ -494,7 +549,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-variant", action="store_true", help="skip the fixed-GOP compensation variant of c2")
+    ap.add_argument("--no-variant", action="store_true", help="skip the fixed-GOP compensation variant of c2 and the CaBR-Net variant of c5")
     ap.add_argument("--streams", type=int, default=1, help="independent clips per GPU (c4: 64 / world)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for the final timing / parity gather (gloo lets ranks share a GPU in tests)")

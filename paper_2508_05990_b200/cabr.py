@@ -341,6 +341,38 @@ def layer_flops(block_size: int, num_classes: int) -> list:
     return layers
 
 
+def _regions(k: int, t0: int, ts: int):
+    """Receptive field of block output rows [t0, t0+ts) per layer (csrc/bmc_cabr.cu regions())."""
+    nd = k // 2 + 1
+    l0 = k // 2 + 2 + t0
+    d0 = ((l0 - 1) >> 2, ((l0 + ts) >> 2) + 1)
+    e2 = (max(d0[0] - 1, 0), min(d0[1] + 1, nd))
+    e1 = (max(e2[0] - 1, 0), min(e2[1] + 1, nd))
+    e0 = (max(2 * e1[0] - 1, 0), min(2 * (e1[1] - 1) + 2, k + 1))
+    return {"e0": e0[1] - e0[0], "e1": e1[1] - e1[0], "e2": e2[1] - e2[0], "d0": d0[1] - d0[0]}
+
+
+def executed_flops(block_size: int, num_classes: int) -> int:
+    """FLOPs the B200 kernel executes per block (2 per multiply-add): every layer only
+    over the receptive field of the cropped K x K logits, per 32 x 32 output tile
+    (the reference's layer_flops counts the full maps)."""
+    _require_kernel_block(block_size)
+    k, c = block_size, num_classes
+    ts = 32 if k >= 32 else 16
+    total = 0
+    for ty in range(0, k, ts):
+        ry = _regions(k, ty, ts)
+        for tx in range(0, k, ts):
+            rx = _regions(k, tx, ts)
+            a = {n: ry[n] * rx[n] for n in ry}
+            total += 2 * 9 * 16 * a["e0"]                     # img_enc.0 (ctx_enc.0 is a table lookup)
+            total += 2 * (2 * 9 * 16 * 32 * a["e1"])          # img/ctx enc.1
+            total += 2 * (2 * 9 * 32 * 32 * a["e2"])          # img/ctx enc.2
+            total += 2 * 9 * 64 * 32 * a["d0"]                # dec.0
+            total += 2 * 9 * 32 * 32 * ts * ts + 2 * 32 * c * ts * ts  # dec.1 + head
+    return total
+
+
 def count_cabr_flops(block_size: int, num_classes: int, invocations: int) -> int:
     """Total flops for ``invocations`` forward passes."""
     if invocations < 0:

@@ -15,8 +15,8 @@
 // about 70% of their maps.  A CTA owns one (flagged block, TS x TS output tile)
 // item (TS = min(K, 32), so shared memory stays bounded for any K); all
 // activations of the item stay in shared memory, each layer's weights are
-// staged into shared memory before the layer (warp-uniform float4 broadcasts in
-// the inner loop), and the arithmetic is plain fp32 FFMA: the reference computes
+// staged into shared memory by cp.async while the previous layer computes
+// (double-buffered; warp-uniform float4 broadcasts in the inner loop), and the arithmetic is plain fp32 FFMA: the reference computes
 // in float32 and its tolerance (1e-5 relative) rules out TF32 tensor cores.
 //
 // The context input is the one-hot map of the predicted labels with the central
@@ -150,14 +150,19 @@ struct CabrArgs {
   CabrGeo g;
 };
 
-__device__ __forceinline__ void stage_weights(float* __restrict__ dst, const float* __restrict__ src, int n) {
-  // packed layer offsets are multiples of 16 floats, so float4 copies are aligned
+// Asynchronous copy of a layer's weights into shared memory (LDGSTS), one commit
+// group; consumed after cp_async_wait_all() + __syncthreads().
+__device__ __forceinline__ void stage_weights_async(float* dst, const float* src, int n) {
   const int n4 = n >> 2;
-  const float4* s4 = reinterpret_cast<const float4*>(src);
-  float4* d4 = reinterpret_cast<float4*>(dst);
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) d4[i] = __ldg(s4 + i);
-  for (int i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16 * i), "l"(src + 4 * i));
+  for (int i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d + 4 * i), "l"(src + i));
+  asm volatile("cp.async.commit_group;\n" ::);
 }
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // out[o][r][c] (region ro x co, plane-major) = relu(bias[o] + sum_{ci, ky, kx}
 // w[ci][ky*3+kx][o] * in[ci][r*stride-1+ky][c*stride-1+kx]), `in` zero outside
@@ -363,7 +368,7 @@ __device__ void dec1_head(const float* __restrict__ d0, Range rd, Range cd, int 
 }
 
 template <int TS, int THREADS>
-__global__ void __launch_bounds__(THREADS, TS == 16 ? 2 : 1) cabr_kernel(const CabrArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) cabr_kernel(const CabrArgs a) {
   extern __shared__ __align__(16) float smem[];
   const CabrGeo& g = a.g;
   const int K = g.K, S = 2 * K + 1, C = a.C;
@@ -374,9 +379,21 @@ __global__ void __launch_bounds__(THREADS, TS == 16 ? 2 : 1) cabr_kernel(const C
   float* sE0 = smem + g.off_e0;
   float* sE1 = smem + g.off_e1;
   float* sE2 = smem + g.off_e2;
-  float* sW = smem + g.off_w;
+  float* sW[2] = {smem + g.off_w, smem + g.off_w + g.wfloats};
   uint8_t* sLab = reinterpret_cast<uint8_t*>(smem) + g.off_lab;
   constexpr int PXD = 2 * TS * TS / THREADS;  // decoder pixels per lane pair
+  // The item's eight weight stages, double-buffered: stage j lands in sW[j & 1]
+  // while the layer before it computes from the other buffer.
+  const float* wsrc[8] = {a.wts + wo.w[0], a.wts + wo.w[1], a.wts + wo.w[2], a.wts + wo.w[4],
+                          a.wts + wo.w[5], a.wts + wo.w[6], a.wts + wo.w[6] + 32 * 9 * 32, a.wts + wo.w[7]};
+  const int wlen[8] = {9 * 16 + 16, 16 * 9 * 32 + 32, 32 * 9 * 32 + 32, 16 * 9 * 32 + 32, 32 * 9 * 32 + 32,
+                       32 * 9 * 32, 32 * 9 * 32 + 32, 32 * 9 * 32 + 32 + C * 32 + C};
+  auto issue = [&](int j) { stage_weights_async(sW[j & 1], wsrc[j], wlen[j]); };
+  auto ready = [&]() {
+    cp_async_wait_all();
+    __syncthreads();
+  };
+  if ((int)blockIdx.x < n_items) issue(0);
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int e = item / per_block, tile = item - e * per_block;
     const int ty0 = (tile / g.tiles) * TS, tx0 = (tile % g.tiles) * TS;
@@ -414,18 +431,17 @@ __global__ void __launch_bounds__(THREADS, TS == 16 ? 2 : 1) cabr_kernel(const C
       }
       sP[i] = v;
     }
-    stage_weights(sW, a.wts + wo.w[0], 9 * 16 + 16);
-    __syncthreads();
+    ready();
+    issue(1);
     // ---- image encoder (cabr.py:228-232)
-    conv3x3<16, 1>(sP, rr.p, rc.p, S, 1, sW, sW + 144, 16, 2, sE0, rr.e0, rc.e0, false, true);
-    __syncthreads();
-    stage_weights(sW, a.wts + wo.w[1], 16 * 9 * 32 + 32);
-    __syncthreads();
-    conv3x3<16, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW, sW + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
-    __syncthreads();
-    stage_weights(sW, a.wts + wo.w[2], 32 * 9 * 32 + 32);
-    __syncthreads();
-    conv3x3<16, 2>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW, sW + 32 * 9 * 32, 32, 1, sE2, rr.e2, rc.e2, false, true);
+    conv3x3<16, 1>(sP, rr.p, rc.p, S, 1, sW[0], sW[0] + 144, 16, 2, sE0, rr.e0, rc.e0, false, true);
+    ready();
+    issue(2);
+    conv3x3<8, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW[1], sW[1] + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
+    ready();
+    issue(3);
+    conv3x3<8, 1>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sE2, rr.e2, rc.e2, false,
+                  true);
     __syncthreads();
     // ---- context encoder
     if (explicit_patch) {
@@ -436,33 +452,30 @@ __global__ void __launch_bounds__(THREADS, TS == 16 ? 2 : 1) cabr_kernel(const C
     } else {
       ctx_conv0_onehot(sLab, rr.p, rc.p, S, K, C, a.wts + wo.w[3], a.wts + wo.b[3], sE0, rr.e0, rc.e0);
     }
-    stage_weights(sW, a.wts + wo.w[4], 16 * 9 * 32 + 32);
-    __syncthreads();
-    conv3x3<16, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW, sW + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
-    __syncthreads();
-    stage_weights(sW, a.wts + wo.w[5], 32 * 9 * 32 + 32);
-    __syncthreads();
+    ready();
+    issue(4);
+    conv3x3<8, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW[1], sW[1] + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
+    ready();
+    issue(5);
     const int ne2 = rr.e2.n() * rc.e2.n();
-    conv3x3<16, 2>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW, sW + 32 * 9 * 32, 32, 1, sE2 + 32 * ne2, rr.e2, rc.e2,
-                   false, true);
-    __syncthreads();
+    conv3x3<8, 1>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sE2 + 32 * ne2, rr.e2, rc.e2,
+                  false, true);
+    ready();
+    issue(6);
     // ---- decoder conv 0 over the 64 fused channels, in two staged halves
     // (image half then context half: one accumulation order, cabr.py:235-237)
     float* sD0 = sE0;  // enc0 maps are dead
-    stage_weights(sW, a.wts + wo.w[6], 32 * 9 * 32);
-    __syncthreads();
-    conv3x3<16, 2>(sE2, rr.e2, rc.e2, K / 2 + 1, 32, sW, nullptr, 32, 1, sD0, rr.d0, rc.d0, false, false);
-    __syncthreads();
-    stage_weights(sW, a.wts + wo.w[6] + 32 * 9 * 32, 32 * 9 * 32 + 32);
-    __syncthreads();
-    conv3x3<16, 2>(sE2 + 32 * ne2, rr.e2, rc.e2, K / 2 + 1, 32, sW, sW + 32 * 9 * 32, 32, 1, sD0, rr.d0, rc.d0,
-                   true, true);
-    __syncthreads();
+    conv3x3<8, 1>(sE2, rr.e2, rc.e2, K / 2 + 1, 32, sW[1], nullptr, 32, 1, sD0, rr.d0, rc.d0, false, false);
+    ready();
+    issue(7);
+    conv3x3<8, 1>(sE2 + 32 * ne2, rr.e2, rc.e2, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sD0, rr.d0, rc.d0,
+                  true, true);
+    ready();
+    if (item + (int)gridDim.x < n_items) issue(0);  // the next item's first layer
     // ---- decoder conv 1 + head + argmax
-    stage_weights(sW, a.wts + wo.w[7], 32 * 9 * 32 + 32 + C * 32 + C);
-    __syncthreads();
-    dec1_head<PXD>(sD0, rr.d0, rc.d0, rr.l0, rc.l0, TS, sW, sW + 32 * 9 * 32, sW + 32 * 9 * 32 + 32,
-                   sW + 32 * 9 * 32 + 32 + C * 32, C, a, e, bx, by, ty0, tx0, stream);
+    float* w7 = sW[1];
+    dec1_head<PXD>(sD0, rr.d0, rc.d0, rr.l0, rc.l0, TS, w7, w7 + 32 * 9 * 32, w7 + 32 * 9 * 32 + 32,
+                   w7 + 32 * 9 * 32 + 32 + C * 32, C, a, e, bx, by, ty0, tx0, stream);
     __syncthreads();
   }
 }
@@ -499,8 +512,8 @@ int plan_cabr(CabrGeo& g, int K, int C) {
   g.off_e0 = g.off_p + fp;
   g.off_e1 = g.off_e0 + fe0;
   g.off_e2 = g.off_e1 + fe1;
-  g.off_w = g.off_e2 + fe2;
-  g.off_lab = 4 * (g.off_w + g.wfloats);
+  g.off_w = g.off_e2 + fe2;  // two weight buffers (double-buffered stages)
+  g.off_lab = 4 * (g.off_w + 2 * g.wfloats);
   g.smem = g.off_lab + ((g.np * g.np + 15) & ~15);
   if (g.smem > 227 * 1024) {
     set_error("CaBR tile needs %d bytes of shared memory", g.smem);

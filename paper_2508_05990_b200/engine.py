@@ -206,7 +206,8 @@ class ClipEngine:
             motion = searched * len(fme.block_sizes) + (2 if self.T >= 2 else 0)
         else:
             motion = (self.T - 1) * (searched * len(fme.block_sizes) + 2)
-        return pack + motion + 1
+        chain = 1 + 3 * self.T if self.cabr is not None else 1  # flag list + (predict, network, write-back) per frame
+        return pack + motion + chain
 
     def _refine(self, lo: int, hi: int) -> None:
         fin = self.levels[-1]

@@ -167,6 +167,9 @@ class ClipSession:
         for every frame; only the key frames' maps are used (reference
         semantics).
 
+    ``weights`` (CabrWeights) runs the CaBR-Net forward pass on the flagged
+    blocks of predicted frames, as ``run_sequence(..., weights)`` does.
+
     Data movement follows the reference's semantics rather than shipping whole
     label stacks: a key frame's output IS its input label map
     (pipeline.py:116-121 appends the injected LabelMap), so it is returned as
@@ -185,12 +188,14 @@ class ClipSession:
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True, chunks: int = 10, lag: int = 2):
+                 bayer: bool = True, chunks: int = 10, lag: int = 2, weights=None):
         if config.refine_enabled and config.fme.block_sizes[-1] * (2 if bayer else 1) < CABR_MIN_BLOCK:
             raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                              f"{config.fme.block_sizes[-1] * (2 if bayer else 1)}-pixel blocks; disable refinement "
                              f"or use larger blocks")
         self.eng = ClipEngine(config, height, width, n_frames, 1, dtype, bayer)
+        if weights is not None and config.refine_enabled:  # CaBR-Net instead of the ring vote
+            self.eng.set_cabr(weights)
         torch = self.eng.torch
         self.torch = torch
         self.pin_raw = torch.empty(tuple(self.eng.raw.shape[1:]), dtype=self.eng.raw.dtype).pin_memory()
@@ -264,6 +269,10 @@ class ClipSession:
         if need:
             ev = torch.cuda.Event()
             with torch.cuda.stream(self.copy_in):
+                if state["chain_done"] is not None and min(need) < f0:
+                    # labels[r] of an earlier chunk's key frame: that chunk's chain (compute
+                    # stream) wrote its slot from key_labels, so the upload must land after it
+                    self.copy_in.wait_event(state["chain_done"])
                 for r in need:
                     # a key in this chunk goes to key_labels (its chain copies it into labels);
                     # one in an earlier chunk was already chained, so it goes straight to labels
@@ -279,6 +288,8 @@ class ClipSession:
             cs.wait_event(ev)
             state["uploaded"].update(need)
         eng._chain(f0, f1)
+        state["chain_done"] = torch.cuda.Event()
+        state["chain_done"].record(cs)
         pred = [i for i in range(f0, f1) if kinds[i - f0] != 0]
         if pred:
             ev = torch.cuda.Event()
@@ -323,7 +334,7 @@ class ClipSession:
         if tensor is None:
             lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
         state = {"tensor": tensor, "lookup": lookup, "kinds": np.full(eng.T, -1, np.int32), "key_host": {},
-                 "uploaded": set(), "h2d": src.numel() * src.element_size(), "d2h": 0}
+                 "uploaded": set(), "h2d": src.numel() * src.element_size(), "d2h": 0, "chain_done": None}
         self.copy_in.wait_stream(torch.cuda.current_stream())  # earlier users of the device buffers are done
         eng._reset_state()
         if eng.cfg.reference_policy == "previous" and eng.T >= 2:

@@ -257,3 +257,36 @@ def test_gpu_cabr_engine_two_streams_equal_single(cuda):
         frames = [Frame(160, 128, c, FrameKind.BAYER_RGGB) for c in clip]
         res = pipeline.run_sequence(frames, {i: l for i, l in enumerate(labels)}, cfg, weights=w)
         np.testing.assert_array_equal(out[s], np.stack([l.classes for l in res.labels]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["k16", "k64"])
+def test_gpu_cabr_clip_session_and_graph_equal_run_sequence(cuda, name):
+    """Host-buffer ClipSession (chunked chain) and a captured engine replay give run_sequence's labels."""
+    from paper_2508_05990_b200 import cabr, pipeline
+    from paper_2508_05990_b200.engine import ClipEngine
+    from paper_2508_05990_b200.frame_io import Frame, FrameKind
+    d = G.load(f"cabr_pipe_{name}.npz")
+    clip, labels = _pipe_clip(name)
+    T, H, W = clip.shape
+    cfg = _pipe_config(name)
+    w = cabr.random_weights(int(d["num_classes"]), seed=int(d["seed"]))
+    want = d["out_labels"]
+    keys = np.stack([l.classes for l in labels])
+    for chunks in (1, 2, T):
+        sess = pipeline.ClipSession(cfg, H, W, T, np.uint8, True, chunks=chunks, weights=w)
+        got, kinds, _, _ = sess.run(clip, cuda.from_numpy(keys))
+        np.testing.assert_array_equal(np.stack(got), want, err_msg=f"chunks={chunks}")
+    eng = ClipEngine(cfg, H, W, T, 1, np.uint8, True)
+    eng.load_frames(clip)
+    eng.key_labels[0].copy_(cuda.from_numpy(keys))
+    eng.set_cabr(w)
+    eng.capture()
+    for _ in range(2):
+        eng.replay()
+    cuda.cuda.synchronize()
+    out = eng.labels[0].cpu().numpy()
+    kinds = eng.kind[0].cpu().numpy()
+    for t in range(T):
+        if kinds[t] != 0:
+            np.testing.assert_array_equal(out[t], want[t], err_msg=f"graph frame {t}")

@@ -37,7 +37,9 @@ __device__ __forceinline__ void record(Stat* st, long long c0, unsigned long lon
 }
 
 // mode 0: pure VABSDIFF4.ACC; 1: pure VABSDIFF.U32.ACC; 2: VABSDIFF4 + SHF 1:1;
-// 3: VABSDIFF4 + PRMT 1:1; 4: IDP.4A; 5: VABSDIFF4 (non-acc) + LOP3 + IADD + LOP3 + IDP (count idiom)
+// 3: VABSDIFF4 + PRMT 1:1; 4: IDP.4A; 5: VABSDIFF4 (non-acc) + LOP3 + IADD + LOP3 + IDP (count idiom);
+// 6: the uint16 SAD word of the search kernels (bmc_internal.cuh sad_word<uint16_t>):
+//    max.u16x2 + min.u16x2 + IADD + IDP.2A per 2 samples
 template <int MODE>
 __global__ void k_alu(uint32_t* out, Stat* st, uint32_t seed) {
   uint32_t acc[NACC], k[NACC];
@@ -55,6 +57,12 @@ __global__ void k_alu(uint32_t* out, Stat* st, uint32_t seed) {
       if (MODE == 2) { uint32_t s = __funnelshift_r(acc[j], k[j], it & 31); acc[j] = vsad4(s, k[j], acc[j]); }
       if (MODE == 3) { uint32_t s = __byte_perm(acc[j], k[j], 0x5432); acc[j] = vsad4(s, k[j], acc[j]); }
       if (MODE == 4) acc[j] = __dp4a(acc[j], k[j], acc[j]);
+      if (MODE == 6) {
+        uint32_t mx, mn;
+        asm volatile("max.u16x2 %0, %1, %2;" : "=r"(mx) : "r"(acc[j]), "r"(k[j]));
+        asm volatile("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(acc[j]), "r"(k[j]));
+        acc[j] = __dp2a_lo(mx - mn, 0x0101u, acc[j]);
+      }
       if (MODE == 5) {
         uint32_t d = __vabsdiffu4(acc[j], k[j]);
         uint32_t t = (d & 0x7f7f7f7fu) + k[(j + 1) & 7];
@@ -123,6 +131,25 @@ __global__ void k_dadd(double* out, Stat* st, double seed) {
   if (s == 1.2345) out[0] = s;
 }
 
+// fp32 FFMA issue rate (the CaBR-Net kernel's roofline denominator)
+__global__ void k_ffma(float* out, Stat* st, float seed) {
+  float acc[NACC];
+#pragma unroll
+  for (int j = 0; j < NACC; ++j) acc[j] = seed * (j + 1) + threadIdx.x;
+  long long c0 = clock64();
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) acc[j] = fmaf(acc[j], 0.999999f, seed);
+  }
+  record(st, c0, t0);
+  float s = 0;
+#pragma unroll
+  for (int j = 0; j < NACC; ++j) s += acc[j];
+  if (s == 1.2345f) out[0] = s;
+}
+
 int main() {
   int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   printf("{\"sms\": %d}\n", sms);
@@ -152,6 +179,7 @@ int main() {
   L("vabsdiff4+prmt", k_alu<3>, NACC, 4.0);
   L("idp4a", k_alu<4>, NACC, 0.0);
   L("count_idiom(5 instr)", k_alu<5>, NACC, 4.0);
+  L("u16_sad_word(vimnmx x2 + iadd + idp2a)", k_alu<6>, NACC, 2.0);
   L("lds128_x1_per4vsad", k_lds<1>, 32.0 / 4, 4.0);
   L("lds128_x1_per8vsad", k_lds<2>, 32.0 / 4, 4.0);
   L("lds128_x1_per16vsad", k_lds<4>, 32.0 / 4, 4.0);
@@ -168,6 +196,22 @@ int main() {
       double ops = (double)grid * block * ITERS * NACC;
       printf("{\"kernel\": \"dadd\", \"rep\": %d, \"mhz\": %.1f, \"lane_ops_per_clk_per_sm\": %.2f, \"Gops_per_s\": %.1f}\n",
              rep, (double)h.cyc / h.ns * 1e3, ops / ((double)h.cyc * sms), ops / (h.ns * 1e-9) / 1e9);
+    }
+  }
+  {
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float* fout; cudaMalloc(&fout, 16);
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaMemset(st, 0, sizeof(Stat));
+      cudaEventRecord(e0);
+      k_ffma<<<grid, block>>>(fout, st, 1.0001f);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      Stat h; cudaMemcpy(&h, st, sizeof(Stat), cudaMemcpyDeviceToHost);
+      double ops = (double)grid * block * ITERS * NACC;
+      printf("{\"kernel\": \"ffma_f32\", \"rep\": %d, \"mhz\": %.1f, \"lane_ops_per_clk_per_sm\": %.2f, "
+             "\"Gops_per_s\": %.1f, \"TFLOPs\": %.2f}\n",
+             rep, (double)h.cyc / h.ns * 1e3, ops / ((double)h.cyc * sms), ops / (h.ns * 1e-9) / 1e9,
+             2 * ops / (h.ns * 1e-9) / 1e12);
     }
   }
   CK(cudaGetLastError());
