@@ -274,6 +274,32 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     }();
     pl.split = (!no_split && pl.per > 1) ? 1 : 0;
   }
+  {
+    // successive-elimination screening (bmc_fme_impl.cuh sea_screen): needs every plane
+    // staged by TMA in one pass; its column sums take P*G*bw uint16 (u8) / uint32 (u16)
+    static const bool no_sea = [] {
+      const char* e = knob_env("BMC_NO_SEA");
+      return e && *e && *e != '0';
+    }();
+    // row stride of the column sums: an odd number of words, so the LB pass (one
+    // thread per candidate row, lanes G rows apart) reads 32 different banks
+    const int vc_eb = eb == 1 ? 2 : 4, vc_words = (pl.bw * vc_eb + 3) / 4;
+    const int vcs = (vc_words | 1) * 4 / vc_eb;
+    const int vc_bytes = p.planes * G * vcs * vc_eb;
+    const int off_vc = (pl.smem + 127) & ~127;
+    // unit-step stages only: on a coarse grid (s > 1) the exact match is rarely a candidate,
+    // so nothing prunes and the bound is pure overhead
+    if (!no_sea && pl.pg == p.planes && p.planes <= 4 && pl.use_tma && s == 1 && G >= 9 && kblk * p.planes <= 32 &&
+        kblk <= 8 && kblk * G <= pl.nmax &&
+        off_vc + vc_bytes <= kSmemBudget) {
+      pl.sea = 1;
+      pl.vcs = vcs;
+      pl.off_vc = off_vc;
+      pl.smem = off_vc + vc_bytes;
+      // past this many exact-SAD survivors (a warp each) the dense screening is cheaper
+      pl.sea_cap = std::max(8, std::min(2 * pl.nmax, kblk * pl.nmax / 10));
+    }
+  }
   static const int debug_skip = [] {
     const char* e = knob_env("BMC_DEBUG_SKIP");
     return e ? atoi(e) : 0;

@@ -44,6 +44,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "bmc_internal.cuh"
 #include "bmc_launch.cuh"
@@ -73,6 +74,11 @@ struct SmemLayout {
   int* klist2;                 // [nmax]
   uint32_t* cur;               // [pg][b][cbw_words]
   uint32_t* win;               // [pg][hwin][bw_words] (+ phase copies at copy_words strides)
+  int* csum;                   // [32] SEA: current-block plane sums (kb * P + p)
+  uint32_t* seaT;              // [8] SEA: smallest exact SAD of the round-1 candidates per block
+  int* seaM;                   // [8] SEA: smallest bound per block (-1: no valid candidate)
+  int* rect;                   // [32] SEA: valid candidate rectangle per block (ilo, ihi, jlo, jhi)
+  void* vc;                    // SEA column sums
 };
 
 __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan& pl) {
@@ -90,6 +96,15 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   L.miscd = reinterpret_cast<double*>(p);
   p += 4 * 8;
   L.bar = reinterpret_cast<unsigned long long*>(p);
+  p += 16;
+  L.csum = reinterpret_cast<int*>(p);
+  p += 32 * 4;
+  L.seaT = reinterpret_cast<uint32_t*>(p);
+  p += 8 * 4;
+  L.seaM = reinterpret_cast<int*>(p);
+  p += 8 * 4;
+  L.rect = reinterpret_cast<int*>(p);
+  L.vc = base + pl.off_vc;
   L.sad = reinterpret_cast<uint32_t*>(base + pl.off_sad);
   L.klist = reinterpret_cast<int*>(base + pl.off_klist);
   L.klist2 = L.klist + pl.nmax;
@@ -98,7 +113,7 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   return L;
 }
 
-static inline int smem_head_bytes() { return 256 * 8 + kMaxSW * 28 + 16 * 4 + 4 * 8 + 16; }
+static inline int smem_head_bytes() { return 256 * 8 + kMaxSW * 28 + 16 * 4 + 4 * 8 + 16 + 32 * 4 + 8 * 4 + 8 * 4 + 32 * 4; }
 
 // ---------------------------------------------------------------------------
 // TMA helpers (inline PTX)
@@ -552,6 +567,227 @@ __device__ int count_lo(const SmemLayout& L, const StagePlan& pl, const StageGeo
   return EPW == 4 ? (cnt + n) / 2 : cnt;
 }
 
+// ---------------------------------------------------------------------------
+// Successive elimination (SEA) screening.  The sum-difference bound
+//   LB(c) = sum_p | sum(cur_p) - sum(ref_p(c)) |  <=  SAD(c)
+// (triangle inequality per CFA plane) costs two box sums per candidate instead
+// of P*b*b absolute differences.  T = exact SAD of the candidate with the
+// smallest LB is >= the minimum SAD, so every candidate that can be the
+// (first) minimum, or tie it, has LB <= T: those get their exact SAD, all others
+// keep LB (> T) in the sum array.  select_block is unchanged and stays exact:
+// its first minimum is over exact values only (the rest exceed T), and every
+// later test (SAD threshold, free sparsity bound, count_lo) only needs a LOWER
+// bound of S, which LB is.  When too many candidates survive (content with no
+// close match) the stage falls back to the dense screening.
+// ---------------------------------------------------------------------------
+template <typename Elem>
+__device__ __forceinline__ uint32_t word_sum(uint32_t v) {
+  if constexpr (sizeof(Elem) == 1) return __dp4a(v, 0x01010101u, 0u);
+  else return (v & 0xffffu) + (v >> 16);
+}
+
+// Exact SAD of the candidate whose window starts at element xo of staged row yo
+// (all P planes staged), warp-cooperative; every lane returns the sum.
+template <typename Elem>
+__device__ uint32_t warp_sad(const SmemLayout& L, const StagePlan& pl, int P, int b, int cur_w0, int xo, int yo) {
+  constexpr int EPW = 4 / sizeof(Elem);
+  const int lane = threadIdx.x & 31;
+  const int lwpr = __ffs(b / EPW) - 1, lb = __ffs(b) - 1;  // b and b/EPW are powers of two
+  const int total = P << (lb + lwpr);
+  const int bww = pl.bw / EPW, cbw = pl.cbw / EPW;
+  const int sh = (xo % EPW) * 8 * (int)sizeof(Elem), w0 = xo / EPW;
+  uint32_t acc = 0;
+  for (int idx = lane; idx < total; idx += 32) {
+    const int w = idx & ((1 << lwpr) - 1), py = idx >> lwpr;  // py = p * b + y
+    const int p = py >> lb, y = py & (b - 1);
+    const uint32_t* rr = L.win + (p * pl.wrows + yo + y) * bww + w0 + w;
+    const uint32_t lo = rr[0];
+    const uint32_t rw = sh ? __funnelshift_r(lo, rr[1], sh) : lo;
+    acc = sad_word(L.cur[py * cbw + cur_w0 + w], rw, acc, Elem());
+  }
+  for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  return acc;
+}
+
+// Returns false (uniformly) when the dense screening must run instead.  Unit-step
+// stages only (the planner enables it for s == 1).
+template <typename Elem, int P>
+__device__ bool sea_screen(const SmemLayout& L, const StageGeom& g, int b, const StagePlan& pl, int coff_w,
+                           int nblk, int ox0, int oy, int frame_w, int frame_h) {
+  using VcT = typename std::conditional<sizeof(Elem) == 1, uint16_t, uint32_t>::type;
+  constexpr int EPW = 4 / sizeof(Elem);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int G = g.G, r = g.r, N = G * G;
+  const int bww = pl.bw / EPW, cbw = pl.cbw / EPW, wpr = b / EPW;
+  const int parts = pl.parts;
+  const FastDiv fG(G, pl.mG);
+  VcT* vc = reinterpret_cast<VcT*>(L.vc);  // [P][G][vcs]
+  // bounds go to the part-0 arrays; later parts must read 0 when select_block folds them
+  for (int k = tid; k < nblk * (parts - 1) * N; k += nt) L.sad[(k / ((parts - 1) * N)) * parts * N + N + k % ((parts - 1) * N)] = 0;
+  if (tid < nblk) {
+    // valid candidates of block kb: i in [ilo, ihi] x j in [jlo, jhi] (fme.py:250-253, step 1)
+    const int ox = ox0 + tid * b;
+    int* rc = L.rect + 4 * tid;
+    rc[0] = max(0, r - (ox + g.cx));
+    rc[1] = min(G - 1, r + (frame_w - b - ox - g.cx));
+    rc[2] = max(0, r - (oy + g.cy));
+    rc[3] = min(G - 1, r + (frame_h - b - oy - g.cy));
+  }
+  // current-block plane sums
+  for (int q = warp; q < nblk * P; q += nw) {
+    const int kb = q / P, p = q - kb * P;
+    uint32_t acc = 0;
+    for (int idx = lane; idx < b * wpr; idx += 32) {
+      const int y = idx / wpr, w = idx - y * wpr;
+      acc += word_sum<Elem>(L.cur[(p * b + y) * cbw + coff_w + kb * wpr + w]);
+    }
+    for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane == 0) L.csum[q] = (int)acc;
+  }
+  // column sums over the b rows of every candidate row offset j, per element column:
+  // a sliding window down the staged rows, all elements of a word at once
+  for (int q = tid; q < P * bww; q += nt) {
+    const int p = q / bww, w = q - p * bww;
+    const uint32_t* col = L.win + p * pl.wrows * bww + w;
+    VcT* dst = vc + p * G * pl.vcs + w * EPW;
+    uint32_t a0 = 0, a1 = 0;
+    auto add = [&](uint32_t v, bool sub) {
+      uint32_t lo, hi;
+      if constexpr (sizeof(Elem) == 1) {
+        lo = v & 0x00ff00ffu;  // bytes 0, 2 in 16-bit lanes (b * 255 < 65536)
+        hi = (v >> 8) & 0x00ff00ffu;
+      } else {
+        lo = v & 0xffffu;
+        hi = v >> 16;
+      }
+      a0 = sub ? a0 - lo : a0 + lo;
+      a1 = sub ? a1 - hi : a1 + hi;
+    };
+    for (int y = 0; y < b - 1; ++y) add(col[y * bww], false);
+    for (int j = 0; j < G; ++j) {
+      add(col[(j + b - 1) * bww], false);
+      if constexpr (sizeof(Elem) == 1) {
+        dst[0] = (VcT)(a0 & 0xffffu);
+        dst[1] = (VcT)(a1 & 0xffffu);
+        dst[2] = (VcT)(a0 >> 16);
+        dst[3] = (VcT)(a1 >> 16);
+      } else {
+        dst[0] = a0;
+        dst[1] = a1;
+      }
+      dst += pl.vcs;
+      add(col[j * bww], true);
+    }
+  }
+  __syncthreads();
+  // LB of every candidate: one thread per (block, candidate row, column chunk)
+  // slides the P box sums along its columns, keeping the smallest bound over valid
+  // columns of the row (chunks combine with atomicMin)
+  uint32_t* rowmin = reinterpret_cast<uint32_t*>(L.klist2);  // [nblk * G]
+  const int nrow = nblk * G;
+  const int nch = max(1, min(4, min(G, nt / nrow)));
+  const int chw = (G + nch - 1) / nch;
+  for (int q = tid; q < nrow; q += nt) rowmin[q] = 0xffffffffu;
+  __syncthreads();
+  for (int t = tid; t < nrow * nch; t += nt) {
+    const int q = t / nch, ch = t - q * nch;
+    uint32_t kb, j;
+    fG.divmod(q, kb, j);
+    const int i0 = ch * chw, i1 = min(G, i0 + chw);
+    if (i0 >= i1) continue;
+    const int* rc = L.rect + 4 * kb;
+    const bool row_ok = (int)j >= rc[2] && (int)j <= rc[3];
+    int box[P], C[P];
+    const VcT* row = vc + j * pl.vcs + g.d + kb * b + i0;  // plane p at + p * G * vcs
+    const int pst = G * pl.vcs;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      box[p] = 0;
+      C[p] = L.csum[kb * P + p];
+    }
+#pragma unroll 4
+    for (int x = 0; x < b; ++x)
+#pragma unroll
+      for (int p = 0; p < P; ++p) box[p] += (int)row[p * pst + x];
+    uint32_t* dst = L.sad + kb * parts * N + j * G;
+    uint32_t mn = 0xffffffffu;
+    const int vlo = row_ok ? rc[0] : G, vhi = row_ok ? rc[1] : -1;
+    for (int i = i0; i < i1; ++i) {
+      if (i > i0) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) box[p] += (int)row[p * pst + i - i0 - 1 + b] - (int)row[p * pst + i - i0 - 1];
+      }
+      uint32_t lb = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) lb += (uint32_t)abs(box[p] - C[p]);
+      dst[i] = lb;
+      if (i >= vlo && i <= vhi) mn = min(mn, lb);
+    }
+    if (mn != 0xffffffffu) atomicMin(rowmin + q, mn);
+  }
+  __syncthreads();
+  // smallest bound per block (L.seaM[kb] = -1: no valid candidate)
+  for (int kb = warp; kb < nblk; kb += nw) {
+    uint32_t mn = 0xffffffffu;
+    for (int j = lane; j < G; j += 32) mn = min(mn, rowmin[kb * G + j]);
+    for (int m = 16; m; m >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, m));
+    if (lane == 0) {
+      const int* rc = L.rect + 4 * kb;
+      L.seaM[kb] = (rc[0] <= rc[1] && rc[2] <= rc[3]) ? (int)mn : -1;
+      L.seaT[kb] = 0xffffffffu;
+    }
+  }
+  if (tid == 0) L.misc[9] = 0;
+  __syncthreads();
+  // Two rounds of exact SADs: (1) every candidate at the smallest bound -- the
+  // exact match, where the content has one, has bound 0 -- giving T = their
+  // smallest SAD; (2) every remaining candidate with bound <= T.  Only rows
+  // whose smallest bound is in range are scanned.
+  for (int round = 0; round < 2; ++round) {
+    for (int q = tid; q < nblk * G; q += nt) {
+      uint32_t kb, j;
+      fG.divmod(q, kb, j);
+      if (L.seaM[kb] < 0) continue;
+      const uint32_t lo = (uint32_t)L.seaM[kb], hi = round == 0 ? lo : L.seaT[kb];
+      if (rowmin[q] > hi || (round == 1 && hi <= lo)) continue;
+      const int* rc = L.rect + 4 * kb;
+      const uint32_t* lbs = L.sad + kb * parts * N + j * G;
+      for (int i = rc[0]; i <= rc[1]; ++i) {
+        const uint32_t v = lbs[i];
+        // round 1 wrote exact SADs (>= their bound == lo) into the array: skip values at lo
+        if (round == 0 ? v != lo : (v <= lo || v > hi)) continue;
+        const int slot = atomicAdd(&L.misc[9], 1);
+        if (slot < pl.sea_cap) L.klist[slot] = (int)(q * G) + i;
+      }
+    }
+    __syncthreads();
+    const int n = L.misc[9];
+    if (n > pl.sea_cap) return false;
+    for (int e = warp; e < n; e += nw) {
+      uint32_t qb, i, kb, j;
+      fG.divmod(L.klist[e], qb, i);
+      fG.divmod(qb, kb, j);
+      const uint32_t sd = warp_sad<Elem>(L, pl, P, b, coff_w + kb * wpr, g.d + kb * b + i, j);
+      if (lane == 0) {
+        L.sad[kb * parts * N + j * G + i] = sd;
+        if (round == 0) atomicMin(&L.seaT[kb], sd);
+      }
+    }
+    __syncthreads();
+    if (round == 0) {
+      // T > 0: no exact match.  Candidates with bounds in (T, sthr] would reach
+      // select_block's contender tests with their bound instead of their SAD and
+      // cost a count_lo each; the dense screening is cheaper for those blocks.
+      bool exact = true;
+      for (int kb = 0; kb < nblk; ++kb) exact &= L.seaM[kb] < 0 || L.seaT[kb] == 0;
+      if (!exact) return false;
+    }
+    if (tid == 0) L.misc[9] = 0;
+    __syncthreads();
+  }
+  return true;
+}
+
 // Staging + integer SAD of one stage for nblk horizontally adjacent blocks
 // sharing one search centre (nblk > 1 only for level 0's first searched stage,
 // whose centre is (0, 0) for every block).  All threads participate.
@@ -592,11 +828,20 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
       tma_load_3d(L.win, tm_win, g.tx0, g.wy0, pc.ref_z, L.bar);
       tma_load_3d(L.cur, tm_cur, cx0, oy, pc.cur_z, L.bar);
     }
-    if (pl.split)
+    if (pl.split && !pl.sea)
       for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
     __syncthreads();
     mbar_wait(L.bar, phase);
     phase ^= 1;
+    if (pl.sea) {
+      const bool done = pc.P == 4 ? sea_screen<Elem, 4>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h)
+                                  : sea_screen<Elem, 1>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h);
+      if (done) return g;
+      if (pl.split) {  // dense fallback: its split tail items accumulate with atomics
+        for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
+        __syncthreads();
+      }
+    }
     sad_items<Elem, CW, TY, SHIFT>(L, g, b, pc.P, pl, coff_w, false, nblk);
     __syncthreads();
     return g;

@@ -30,6 +30,10 @@ struct StagePlan {
   unsigned long long mG, mncg, mrho, mcpr, ms, mparts, mgw, mcells, mper;
   int split;      // split the partial last warp's items into one-unit sub-items (single-pass plans)
   int per;        // units per part (single-pass plans), 0 = compute on device
+  int sea;        // 1: successive-elimination screening first (dense screening only as fallback)
+  int off_vc;     // byte offset of the SEA column-sum region ([P][G][bw] uint16 (u8) / uint32 (u16))
+  int sea_cap;    // max survivors per CTA before falling back to dense screening
+  int vcs;        // SEA column-sum row stride (elements; an odd number of 32-bit words: no bank conflicts)
 };
 
 #ifndef BMC_STAGE_THREADS

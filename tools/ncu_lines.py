@@ -32,3 +32,6 @@ tot = sum(v[0] for v in agg.values()); ts = sum(v[1] for v in agg.values())
 print(f"total warp instructions {tot:.4g}")
 for (f, l), (n, s, src) in sorted(agg.items(), key=lambda x: -x[1][0])[:int(sys.argv[2]) if len(sys.argv) > 2 else 30]:
     print(f"{100*n/tot:5.1f}% inst {100*s/max(ts,1):5.1f}% stall  {f}:{l}  {src.strip()[:90]}")
+print("-- by stall samples")
+for (f, l), (n, s, src) in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 30]:
+    print(f"{100*n/tot:5.1f}% inst {100*s/max(ts,1):5.1f}% stall  {f}:{l}  {src.strip()[:90]}")
