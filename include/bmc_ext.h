@@ -137,6 +137,71 @@ int bmc_cabr_chain(uint8_t* labels, int64_t frame_stride, int64_t stream_stride,
                    int64_t pix_stream_stride, int num_classes, const float* packed, uint8_t* scratch,
                    int32_t* workspace, void* stream);
 
+/* --------------------------------------------------------------- session --
+ * Native executor of the host-buffer clip pipeline (ClipSession.run with the
+ * "previous" reference policy and key maps in one pinned (T, Hl, Wl) host
+ * array): the clip is processed in n_chunks frame ranges, software-pipelined
+ * `lag` chunks deep on three streams --
+ *   copy_in : H2D of a chunk's raw frames, then of the key maps its predicted
+ *             frames reference (only those, once);
+ *   compute : pack, ME, MV refinement, AEM scan of the chunk's pairs
+ *             (bmc_pack_planes / bmc_estimate_motion / bmc_refine_mvs /
+ *             bmc_decide), later the chunk's label chain (bmc_predict_labels_clip,
+ *             or bmc_cabr_chain when cabr_packed is set);
+ *   copy_out: D2H of the decisions, then of the predicted frames' labels.
+ * The host reads each chunk's decisions (event wait) `lag` chunks behind the
+ * GPU to pick the key maps to upload -- the same data movement as the Python
+ * orchestration, without its per-call overhead.  Every pointer is caller-owned;
+ * bmc_session_init allocates the events (priv), bmc_session_destroy frees them. */
+#define BMC_SESSION_MAX_CHUNKS 64
+typedef struct bmc_session {
+  int32_t T, H, W, elem_bytes, kind;                  /* frames; raw frame geometry; BMC kind of bmc_pack_planes */
+  int32_t n_chunks, lag;
+  int32_t chunk_begin[BMC_SESSION_MAX_CHUNKS + 1];    /* frame ranges [chunk_begin[c], chunk_begin[c+1]) */
+  int32_t gh, gw, b_final, scale, deviation_threshold, n_levels, Hl, Wl, ring_vote;
+  bmc_fme_params params;
+  bmc_select_params select;
+  /* device buffers (one stream of a clip engine, pair p = frame p+1) */
+  void* raw;
+  void* planes;
+  const int32_t* cur_index;
+  const int32_t* ref_index;
+  bmc_level_out levels[BMC_MAX_LEVELS];
+  int32_t* mv_ref;
+  double* e_ref;
+  int32_t* replaced;
+  void* aem_state;                                    /* zeroed per run (acc, trigger, fsk, last_key, kind) */
+  int64_t aem_state_bytes;
+  double* acc;
+  int32_t* fsk;
+  int32_t* last_key;
+  int32_t* kind_out;
+  int32_t* ref_out;                                   /* filled with -1 per run */
+  double* trigger;
+  uint8_t* labels;                                    /* (T, Hl, Wl) */
+  uint8_t* key_labels;                                /* (T, Hl, Wl) */
+  uint32_t* chain_ws;
+  const float* cabr_packed;                           /* NULL: ring vote / plain prediction */
+  int32_t cabr_classes;
+  uint8_t* cabr_scratch;
+  int32_t* cabr_ws;
+  /* pinned host buffers */
+  const void* host_raw;                               /* (T, H, W) */
+  const uint8_t* host_keys;                           /* (T, Hl, Wl) */
+  uint8_t* host_labels;                               /* (T, Hl, Wl): predicted frames written */
+  int32_t* host_kind;
+  int32_t* host_ref;
+  double* host_trigger;
+  void* compute;
+  void* copy_in;
+  void* copy_out;
+  int64_t h2d_bytes, d2h_bytes;                       /* of the last run */
+  void* priv;
+} bmc_session;
+int bmc_session_init(bmc_session* s);
+int bmc_session_run(bmc_session* s);
+void bmc_session_destroy(bmc_session* s);
+
 #ifdef __cplusplus
 }
 #endif

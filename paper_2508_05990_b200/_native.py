@@ -48,6 +48,27 @@ class SelectParams(ctypes.Structure):
     ]
 
 
+class Session(ctypes.Structure):
+    """Mirror of ``bmc_session`` (include/bmc_ext.h): the native chunked clip executor."""
+
+    MAX_CHUNKS = 64
+    _fields_ = [
+        ("T", i32), ("H", i32), ("W", i32), ("elem_bytes", i32), ("kind", i32), ("n_chunks", i32), ("lag", i32),
+        ("chunk_begin", i32 * 65),
+        ("gh", i32), ("gw", i32), ("b_final", i32), ("scale", i32), ("deviation_threshold", i32),
+        ("n_levels", i32), ("Hl", i32), ("Wl", i32), ("ring_vote", i32),
+        ("params", FmeParams), ("select", SelectParams),
+        ("raw", vp), ("planes", vp), ("cur_index", vp), ("ref_index", vp), ("levels", LevelOut * MAX_LEVELS),
+        ("mv_ref", vp), ("e_ref", vp), ("replaced", vp), ("aem_state", vp), ("aem_state_bytes", i64),
+        ("acc", vp), ("fsk", vp), ("last_key", vp), ("kind_out", vp), ("ref_out", vp), ("trigger", vp),
+        ("labels", vp), ("key_labels", vp), ("chain_ws", vp),
+        ("cabr_packed", vp), ("cabr_classes", i32), ("cabr_scratch", vp), ("cabr_ws", vp),
+        ("host_raw", vp), ("host_keys", vp), ("host_labels", vp), ("host_kind", vp), ("host_ref", vp),
+        ("host_trigger", vp), ("compute", vp), ("copy_in", vp), ("copy_out", vp),
+        ("h2d_bytes", i64), ("d2h_bytes", i64), ("priv", vp),
+    ]
+
+
 _SIGNATURES = {
     "bmc_version": (ctypes.c_char_p, []),
     "bmc_abi_version": (ctypes.c_int, []),
@@ -94,6 +115,9 @@ _SIGNATURES = {
     "bmc_refine_blocks": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp]),
     "bmc_cabr_chain_workspace": (ctypes.c_size_t, [ctypes.c_int] * 4),
+    "bmc_session_init": (ctypes.c_int, [ctypes.POINTER(Session)]),
+    "bmc_session_run": (ctypes.c_int, [ctypes.POINTER(Session)]),
+    "bmc_session_destroy": (None, [ctypes.POINTER(Session)]),
     "bmc_cabr_chain": (ctypes.c_int, [vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, i64,
                                       ctypes.c_int, ctypes.c_int, vp, i64, i64, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int, i64, i64, ctypes.c_int, vp,
@@ -138,7 +162,7 @@ def load(build_if_missing: bool = True):
         abi = lib.bmc_abi_version()
         if abi != ABI_VERSION:
             raise ImportError(f"{_LIB_PATH} has ABI {abi}, the Python binding expects {ABI_VERSION}; rebuild it")
-        for code, st in ((0, FmeParams), (1, LevelOut), (2, SelectParams)):
+        for code, st in ((0, FmeParams), (1, LevelOut), (2, SelectParams), (3, Session)):
             if lib.bmc_struct_size(code) != ctypes.sizeof(st):
                 raise ImportError(f"{_LIB_PATH}: {st.__name__} is {lib.bmc_struct_size(code)} bytes in C, "
                                   f"{ctypes.sizeof(st)} in the binding; rebuild it")

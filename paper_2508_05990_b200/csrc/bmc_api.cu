@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "../../include/bmc_ext.h"
 #include "bmc_internal.cuh"
 #include "bmc_launch.cuh"
 
@@ -74,6 +75,7 @@ size_t bmc_struct_size(int which) {
     case 0: return sizeof(bmc_fme_params);
     case 1: return sizeof(bmc_level_out);
     case 2: return sizeof(bmc_select_params);
+    case 3: return sizeof(bmc_session);
     default: return 0;
   }
 }

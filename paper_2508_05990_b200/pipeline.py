@@ -188,7 +188,7 @@ class ClipSession:
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True, chunks: int = 10, lag: int = 2, weights=None):
+                 bayer: bool = True, chunks: int = 5, lag: int = 2, weights=None):
         if config.refine_enabled and config.fme.block_sizes[-1] * (2 if bayer else 1) < CABR_MIN_BLOCK:
             raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                              f"{config.fme.block_sizes[-1] * (2 if bayer else 1)}-pixel blocks; disable refinement "
@@ -211,6 +211,71 @@ class ClipSession:
         self.lag = max(1, int(lag))
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        self._native = self._native_session() if (config.reference_policy == "previous" and t >= 2
+                                                  and len(self.chunks) <= N.Session.MAX_CHUNKS) else None
+
+    def _native_session(self):
+        """bmc_session over this session's device and pinned buffers (include/bmc_ext.h): the
+        chunk schedule of run() for key maps given as one tensor, executed natively."""
+        eng, torch = self.eng, self.torch
+        s = N.Session()
+        s.T, s.H, s.W = eng.T, eng.H, eng.W
+        s.elem_bytes, s.kind = eng.raw.element_size(), eng.kind_code
+        s.n_chunks, s.lag = len(self.chunks), self.lag
+        for k, (f0, _f1) in enumerate(self.chunks):
+            s.chunk_begin[k] = f0
+        s.chunk_begin[len(self.chunks)] = self.chunks[-1][1]
+        s.gh, s.gw, s.b_final, s.scale = eng.gh, eng.gw, eng.b_final, eng.scale
+        s.deviation_threshold = int(eng.cfg.deviation_threshold)
+        s.n_levels, s.Hl, s.Wl, s.ring_vote = len(eng.levels), eng.Hl, eng.Wl, int(eng.ring_vote)
+        s.params, s.select = eng.params, eng.sp
+        s.raw, s.planes = N.ptr(eng.raw), N.ptr(eng.planes)
+        s.cur_index, s.ref_index = N.ptr(eng.cur_index), N.ptr(eng.ref_index)
+        for k, lv in enumerate(eng.levels):
+            s.levels[k] = N.LevelOut(N.ptr(lv.mv), N.ptr(lv.energy), N.ptr(lv.matched), N.ptr(lv.evals))
+        s.mv_ref, s.e_ref, s.replaced = N.ptr(eng.mv_ref), N.ptr(eng.e_ref), N.ptr(eng.replaced)
+        s.aem_state, s.aem_state_bytes = N.ptr(eng._aem_zero), eng._aem_zero.numel()
+        s.acc, s.fsk, s.last_key = N.ptr(eng.acc), N.ptr(eng.fsk), N.ptr(eng.last_key)
+        s.kind_out, s.ref_out, s.trigger = N.ptr(eng.kind), N.ptr(eng.ref), N.ptr(eng.trigger)
+        s.labels, s.key_labels, s.chain_ws = N.ptr(eng.labels), N.ptr(eng.key_labels), N.ptr(eng.workspace)
+        if eng.cabr is not None:
+            c = eng.cabr
+            s.cabr_packed, s.cabr_classes = N.ptr(c["packed"]), c["C"]
+            s.cabr_scratch, s.cabr_ws = N.ptr(c["scratch"]), N.ptr(c["workspace"])
+        self.host_kind = torch.empty(eng.T, dtype=torch.int32).pin_memory()
+        self.host_ref = torch.empty(eng.T, dtype=torch.int32).pin_memory()
+        self.host_trigger = torch.empty(eng.T, dtype=torch.float64).pin_memory()
+        s.host_labels = N.ptr(self.pin_labels)
+        s.host_kind, s.host_ref, s.host_trigger = N.ptr(self.host_kind), N.ptr(self.host_ref), N.ptr(self.host_trigger)
+        s.copy_in, s.copy_out = N.stream_handle(self.copy_in), N.stream_handle(self.copy_out)
+        N.check(N.load().bmc_session_init(ctypes.byref(s)))
+        self._pin_labels_np = self.pin_labels.numpy()
+        return s
+
+    def __del__(self):
+        s = getattr(self, "_native", None)
+        if s is not None and s.priv:
+            try:
+                N.load().bmc_session_destroy(ctypes.byref(s))
+            except Exception:  # interpreter shutdown: module globals already cleared
+                pass
+
+    def _run_native(self, src, keys):
+        """One clip through bmc_session_run (key maps as one pinned (T, Hl, Wl) tensor)."""
+        eng, torch = self.eng, self.torch
+        if not (keys.is_pinned() and keys.is_contiguous() and keys.dtype == torch.uint8):
+            self.pin_key.copy_(keys)
+            keys = self.pin_key
+        s = self._native
+        s.host_raw, s.host_keys = src.data_ptr(), keys.data_ptr()
+        s.compute = N.stream_handle()
+        N.check(N.load().bmc_session_run(ctypes.byref(s)))
+        kinds, refs = self.host_kind.numpy().copy(), self.host_ref.numpy().copy()
+        trig = self.host_trigger.numpy().copy()
+        keys_np, pred_np = keys.numpy(), self._pin_labels_np
+        labels = [keys_np[i] if kinds[i] == 0 else pred_np[i] for i in range(eng.T)]
+        self.h2d_bytes, self.d2h_bytes = int(s.h2d_bytes), int(s.d2h_bytes)
+        return labels, kinds, refs, trig
 
     # -- helpers ----------------------------------------------------------------
     def _motion_chunk(self, src, f0: int, f1: int) -> None:
@@ -330,6 +395,8 @@ class ClipSession:
         tensor = key_labels if isinstance(key_labels, torch.Tensor) else None
         if tensor is not None and tuple(tensor.shape) != tuple(eng.labels.shape[1:]):
             raise ValueError(f"key label tensor must be {tuple(eng.labels.shape[1:])}, got {tuple(tensor.shape)}")
+        if tensor is not None and self._native is not None:
+            return self._run_native(src, tensor)
         lookup = None
         if tensor is None:
             lookup = key_labels if callable(key_labels) else (lambda i: key_labels[i])
