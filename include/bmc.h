@@ -69,7 +69,7 @@ typedef struct bmc_level_out {
 const char* bmc_version(void);
 int bmc_abi_version(void);          /* == BMC_ABI_VERSION of the build                     */
 size_t bmc_struct_size(int which);  /* sizeof: 0 bmc_fme_params, 1 bmc_level_out, 2 bmc_select_params,
-                                       3 bmc_session (bmc_ext.h) */
+                                       3 the session struct of bmc_ext.h */
 /* Byte fill of device memory on `stream` (state resets inside captured steps). */
 int bmc_memset_async(void* dst, int value, size_t bytes, void* stream);
 const char* bmc_last_error(void);

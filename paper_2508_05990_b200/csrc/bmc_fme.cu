@@ -289,7 +289,7 @@ int plan_stage(StagePlan& pl, const bmc_fme_params& p, int b, int r, int s, bool
     const int off_vc = (pl.smem + 127) & ~127;
     // unit-step stages only: on a coarse grid (s > 1) the exact match is rarely a candidate,
     // so nothing prunes and the bound is pure overhead
-    if (!no_sea && pl.pg == p.planes && p.planes <= 4 && pl.use_tma && s == 1 && G >= 9 && kblk * p.planes <= 32 &&
+    if (!no_sea && p.one_minus_lam > 0.0 && pl.pg == p.planes && p.planes <= 4 && pl.use_tma && s == 1 && G >= 9 && kblk * p.planes <= 32 &&
         kblk <= 8 && kblk * G <= pl.nmax &&
         off_vc + vc_bytes <= kSmemBudget) {
       pl.sea = 1;

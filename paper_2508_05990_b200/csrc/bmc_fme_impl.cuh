@@ -78,6 +78,7 @@ struct SmemLayout {
   uint32_t* seaT;              // [8] SEA: smallest exact SAD of the round-1 candidates per block
   int* seaM;                   // [8] SEA: smallest bound per block (-1: no valid candidate)
   int* rect;                   // [32] SEA: valid candidate rectangle per block (ilo, ihi, jlo, jhi)
+  int* seaK0;                  // [8] SEA: first candidate (canonical order) with SAD 0 per block
   void* vc;                    // SEA column sums
 };
 
@@ -104,6 +105,8 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   L.seaM = reinterpret_cast<int*>(p);
   p += 8 * 4;
   L.rect = reinterpret_cast<int*>(p);
+  p += 32 * 4;
+  L.seaK0 = reinterpret_cast<int*>(p);
   L.vc = base + pl.off_vc;
   L.sad = reinterpret_cast<uint32_t*>(base + pl.off_sad);
   L.klist = reinterpret_cast<int*>(base + pl.off_klist);
@@ -113,7 +116,9 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, const StagePlan
   return L;
 }
 
-static inline int smem_head_bytes() { return 256 * 8 + kMaxSW * 28 + 16 * 4 + 4 * 8 + 16 + 32 * 4 + 8 * 4 + 8 * 4 + 32 * 4; }
+static inline int smem_head_bytes() {
+  return 256 * 8 + kMaxSW * 28 + 16 * 4 + 4 * 8 + 16 + 32 * 4 + 8 * 4 + 8 * 4 + 32 * 4 + 8 * 4;
+}
 
 // ---------------------------------------------------------------------------
 // TMA helpers (inline PTX)
@@ -735,6 +740,7 @@ __device__ bool sea_screen(const SmemLayout& L, const StageGeom& g, int b, const
       const int* rc = L.rect + 4 * kb;
       L.seaM[kb] = (rc[0] <= rc[1] && rc[2] <= rc[3]) ? (int)mn : -1;
       L.seaT[kb] = 0xffffffffu;
+      L.seaK0[kb] = 0x7fffffff;
     }
   }
   if (tid == 0) L.misc[9] = 0;
@@ -771,6 +777,7 @@ __device__ bool sea_screen(const SmemLayout& L, const StageGeom& g, int b, const
       if (lane == 0) {
         L.sad[kb * parts * N + j * G + i] = sd;
         if (round == 0) atomicMin(&L.seaT[kb], sd);
+        if (sd == 0) atomicMin(&L.seaK0[kb], (int)(j * G + i));
       }
     }
     __syncthreads();
@@ -786,6 +793,27 @@ __device__ bool sea_screen(const SmemLayout& L, const StageGeom& g, int b, const
     __syncthreads();
   }
   return true;
+}
+
+// Result of a block the SEA screening settled: every block it accepts has an
+// exact match (minimum SAD 0), so with lam < 1 the answer is the first
+// zero-SAD candidate in canonical order with energy 0.0 (select_block's
+// zero-SAD exit, fme.py:266) -- no pass over the candidate sums is needed.
+__device__ __forceinline__ StageResult sea_result(const SmemLayout& L, const StageGeom& g, int kb) {
+  StageResult res;
+  const int* rc = L.rect + 4 * kb;
+  const int k = L.seaK0[kb];
+  if (L.seaM[kb] < 0) {  // no valid candidate
+    res.nvalid = 0;
+    res.dx = res.dy = 0;
+    res.energy = 0.0;
+    return res;
+  }
+  res.nvalid = (rc[1] - rc[0] + 1) * (rc[3] - rc[2] + 1);
+  res.dx = g.cx + (k % g.G - g.r) * g.s;
+  res.dy = g.cy + (k / g.G - g.r) * g.s;
+  res.energy = 0.0;
+  return res;
 }
 
 // Staging + integer SAD of one stage for nblk horizontally adjacent blocks
@@ -819,6 +847,7 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
     for (int i = 0; i < min(g.G, EPW); ++i) phase_mask |= 1u << ((g.d + i * s) % EPW);
 
   __syncthreads();  // previous users of smem are done; mbarrier init visible
+  if (tid == 0) L.misc[10] = 0;  // set to 1 below when the SEA screening settles the stage
   if (pl.use_tma && pl.pg == pc.P && !(phase_mask & ~1u) && !pl.debug) {
     // common case, one TMA pass: clear the atomic-accumulated sums while the
     // boxes are in flight; each thread's mbarrier wait then makes the staged
@@ -836,7 +865,11 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
     if (pl.sea) {
       const bool done = pc.P == 4 ? sea_screen<Elem, 4>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h)
                                   : sea_screen<Elem, 1>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h);
-      if (done) return g;
+      if (done) {
+        if (tid == 0) L.misc[10] = 1;
+        __syncthreads();
+        return g;
+      }
       if (pl.split) {  // dense fallback: its split tail items accumulate with atomics
         for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
         __syncthreads();
@@ -1075,6 +1108,7 @@ __device__ StageResult stage_search(const SmemLayout& L, const PairCtx<Elem>& pc
   int coff_e;
   const StageGeom g = stage_sad<Elem, CW, TY, SHIFT>(L, pc, pl, tm_win, tm_cur, phase, ox, oy, b, cx, cy, r, s, 1,
                                                      coff_e);
+  if (pl.sea && L.misc[10]) return sea_result(L, g, 0);
   return select_block<Elem, CW, TY, SHIFT>(L, pc, pl, g, L.sad, ox, oy, b, coff_e);
 }
 
@@ -1137,8 +1171,10 @@ __global__ void __launch_bounds__(kMaxStageThreads, BMC_STAGE_MINB)
       for (int kb = 0; kb < nb; ++kb) {
         StageGeom gk = g;
         gk.d += kb * b;
-        const StageResult res = select_block<Elem, CW, TY, SHIFT>(L, pc, a.plan, gk, L.sad + kb * nsad, ox0 + kb * b,
-                                                                  oy, b, coff_e + kb * b, kb);
+        const StageResult res = (a.plan.sea && L.misc[10])
+                                    ? sea_result(L, g, kb)
+                                    : select_block<Elem, CW, TY, SHIFT>(L, pc, a.plan, gk, L.sad + kb * nsad,
+                                                                        ox0 + kb * b, oy, b, coff_e + kb * b, kb);
         if (threadIdx.x == 0) {
           const long long c = (long long)pair * cells + (long long)gy * a.gw + gx0 + kb;
           a.mv[2 * c] = res.dx;
