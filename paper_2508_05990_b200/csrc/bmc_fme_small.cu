@@ -54,7 +54,11 @@ __device__ __forceinline__ void word_sc(uint32_t cw, uint32_t rw, uint32_t& S, u
 
 // (S, C_lo) of one candidate: P planes x b rows of WPR words, reference rows
 // read through L1 with one funnel shift per word (shift 0 for aligned rows).
-template <typename Elem, int WPR, bool HIGHD>
+// ALIGNED: the row starts on a WPR*4-byte boundary (every candidate of a stage
+// whose step is a multiple of the block row width, e.g. the coarse s = 8 stage
+// of 8x8 blocks): one vector load per row, no shifts.  Plane strides and the
+// row pitch are 16-byte multiples, so the alignment holds for every row.
+template <typename Elem, int WPR, bool HIGHD, bool ALIGNED>
 __device__ __forceinline__ void cand_sc(const uint32_t* __restrict__ rrow, long long rpitch_w, long long rplane_w,
                                         const uint32_t* crow, int P, int b, int sh, uint32_t k1, uint32_t k2,
                                         uint32_t& S, uint32_t& C, uint32_t& a2) {
@@ -62,8 +66,16 @@ __device__ __forceinline__ void cand_sc(const uint32_t* __restrict__ rrow, long 
     const uint32_t* rr = rrow + pl * rplane_w;
     for (int y = 0; y < b; ++y) {
       uint32_t w[WPR + 1];
+      if constexpr (ALIGNED && WPR == 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(rr));
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; w[4] = 0;
+      } else if constexpr (ALIGNED) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(rr));
+        w[0] = v.x; w[1] = v.y; w[2] = 0;
+      } else {
 #pragma unroll
-      for (int q = 0; q <= WPR; ++q) w[q] = __ldg(rr + q);
+        for (int q = 0; q <= WPR; ++q) w[q] = __ldg(rr + q);
+      }
       uint32_t c[WPR];
       if constexpr (WPR == 4) {
         const uint4 v = *reinterpret_cast<const uint4*>(crow);
@@ -73,7 +85,8 @@ __device__ __forceinline__ void cand_sc(const uint32_t* __restrict__ rrow, long 
         c[0] = v.x; c[1] = v.y;
       }
 #pragma unroll
-      for (int q = 0; q < WPR; ++q) word_sc<Elem, HIGHD>(c[q], __funnelshift_r(w[q], w[q + 1], sh), S, C, k1, k2, a2);
+      for (int q = 0; q < WPR; ++q)
+        word_sc<Elem, HIGHD>(c[q], ALIGNED ? w[q] : __funnelshift_r(w[q], w[q + 1], sh), S, C, k1, k2, a2);
       rr += rpitch_w;
       crow += WPR;
     }
@@ -144,12 +157,23 @@ __device__ SmallStage small_stage(const Elem* __restrict__ cur_g, const Elem* __
     uint32_t S = 0, Cacc = 0, a2 = 0;
     const uint32_t* rrow = reinterpret_cast<const uint32_t*>(ref + (long long)(oy + dy) * p.pitch) + xr / EPW;
     const long long rpw = p.pitch / EPW, rplw = p.plane_stride / EPW;
+    const bool al = sh == 0 && (reinterpret_cast<uintptr_t>(rrow) & (wpr * 4 - 1)) == 0;
     if (wpr == 4) {
-      if (highd) cand_sc<Elem, 4, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
-      else cand_sc<Elem, 4, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      if (al) {
+        if (highd) cand_sc<Elem, 4, true, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+        else cand_sc<Elem, 4, false, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      } else {
+        if (highd) cand_sc<Elem, 4, true, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+        else cand_sc<Elem, 4, false, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      }
     } else {
-      if (highd) cand_sc<Elem, 2, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
-      else cand_sc<Elem, 2, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      if (al) {
+        if (highd) cand_sc<Elem, 2, true, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+        else cand_sc<Elem, 2, false, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      } else {
+        if (highd) cand_sc<Elem, 2, true, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+        else cand_sc<Elem, 2, false, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
+      }
     }
     int C = EPW == 4 ? ((int)Cacc - (int)a2 + n) / 2 : (int)Cacc;
     if (!count) C = 0;

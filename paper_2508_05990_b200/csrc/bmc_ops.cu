@@ -5,6 +5,7 @@
 #include <cstdio>
 
 #include <algorithm>
+#include <mutex>
 
 #include "bmc_internal.cuh"
 #include "bmc_launch.cuh"
@@ -131,19 +132,26 @@ int launch_pack(const void* raw, int n_frames, int kind, const bmc_fme_params& p
 // ---------------------------------------------------------------------------
 // fl(v / 65535) table for the uint16 exact replay.
 // ---------------------------------------------------------------------------
-__global__ void norm_table_kernel(double* tab, int n, double s) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < n) tab[v] = __ddiv_rn((double)v, s);
-}
 
+// One table per device, built once under a lock.  The values are computed on
+// the host (IEEE division is correctly rounded there too, so fl(v/65535) is the
+// same double) and copied synchronously: no kernel on the legacy stream and no
+// device-wide sync, so a later call cannot disturb another stream's work.  The
+// first call must not happen inside a graph capture (the engines warm up first).
 const double* norm_table_u16(int device) {
+  static std::mutex mu;
   static double* tabs[64] = {nullptr};
   if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
   if (!tabs[device]) {
+    static double host[65536];
+    for (int v = 0; v < 65536; ++v) host[v] = (double)v / 65535.0;
     double* t = nullptr;
     if (cudaMalloc(&t, 65536 * sizeof(double)) != cudaSuccess) return nullptr;
-    norm_table_kernel<<<256, 256>>>(t, 65536, 65535.0);
-    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    if (cudaMemcpy(t, host, sizeof host, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(t);
+      return nullptr;
+    }
     tabs[device] = t;
   }
   return tabs[device];
