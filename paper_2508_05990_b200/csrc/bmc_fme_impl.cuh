@@ -488,6 +488,25 @@ __device__ __forceinline__ double exact_cand(const SmemLayout& L, const StagePla
       .energy;
 }
 
+// Partial exact replay of candidate (i, j) over chain groups [q0, q1) (see
+// exact_partial): lets the CTA split one large replay across warps.
+template <typename Elem>
+__device__ __forceinline__ void exact_cand_partial(const SmemLayout& L, const StagePlan& pl, const StageGeom& g,
+                                                   const PairCtx<Elem>& pc, int ox, int oy, int b, int coff, int i,
+                                                   int j, int dx, int dy, int q0, int q1, double& total, int& cnt) {
+  if (pl.pg == pc.P) {
+    const Elem* cur = reinterpret_cast<const Elem*>(L.cur) + coff;
+    const Elem* ref = reinterpret_cast<const Elem*>(L.win) + (long long)(j * g.s) * pl.bw + g.d + i * g.s;
+    exact_partial<Elem>(cur, pl.cbw, (long long)b * pl.cbw, ref, pl.bw, (long long)pl.wrows * pl.bw, b, pc.P, pc.tab,
+                        pc.tol, q0, q1, total, cnt);
+    return;
+  }
+  const long long roff = (long long)(oy + dy) * pc.pitch + (ox + dx);
+  const long long coffg = (long long)oy * pc.pitch + ox;
+  exact_partial<Elem>(pc.cur + coffg, pc.pitch, pc.plane_stride, pc.ref + roff, pc.pitch, pc.plane_stride, b, pc.P,
+                      pc.tab, pc.tol, q0, q1, total, cnt);
+}
+
 // Integer lower bound of the sparsity count of candidate (i, j): #(|r-c| >= D),
 // warp-cooperative over packed 32-bit words (staged tiles, or global planes
 // when not every plane is staged).  uint8: one VABSDIFF4 (per-byte |r-c|) and
@@ -995,12 +1014,49 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     for (int v = tid; v < 256; v += nt) L.tab[v] = __ddiv_rn((double)v, (double)pc.max_value);
   __syncthreads();
   const double unit = (double)pc.max_value * (double)n;
+  // exact energy of the min-SAD candidate: numpy's pairwise tree over n samples
+  // is perfect, so W warps (a power of two dividing the chain-group count) each
+  // take an aligned subtree and warp 0 joins the W subtree sums in tree order
+  const int nq = n > 512 ? n / 512 : 1;  // chain groups: (n / 128 leaves) * 8 chains / 32 lanes
+  int W = 1;
+  while (2 * W <= nw && 2 * W <= nq) W *= 2;
+  if (W > 1) {
+    if (warp < W) {
+      int dx, dy;
+      const int mi = (int)((m0) - fGG.div(m0) * g.G), mj = (int)fGG.div(m0);
+      cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, mi, mj, dx, dy);
+      double tsum;
+      int tcnt;
+      exact_cand_partial<Elem>(L, pl, g, pc, ox, oy, b, coff_e, mi, mj, dx, dy, warp * (nq / W), (warp + 1) * (nq / W),
+                               tsum, tcnt);
+      if (lane == 0) {
+        L.best_e[warp] = tsum;
+        L.best_k[warp] = tcnt;
+      }
+    }
+    __syncthreads();
+  }
   if (warp == 0) {
     double e0 = 0.0;
     if (sad0 != 0) {
-      int dx, dy;
-      cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), dx, dy);
-      e0 = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), dx, dy);
+      if (W > 1) {
+        if (lane == 0) {
+          double v[kMaxSW];
+          int cnt = 0;
+          for (int w = 0; w < W; ++w) {
+            v[w] = L.best_e[w];
+            cnt += L.best_k[w];
+          }
+          for (int st = 1; st < W; st *= 2)
+            for (int w = 0; w + st < W; w += 2 * st) v[w] = __dadd_rn(v[w], v[w + st]);
+          e0 = exact_finish(v[0], cnt, n, pc.oml, pc.lam).energy;
+        }
+      } else {
+        int dx, dy;
+        cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), dx, dy);
+        e0 = exact_cand<Elem>(L, pl, g, pc, ox, oy, b, coff_e, (int)((m0) - fGG.div(m0) * g.G), (int)fGG.div(m0), dx,
+                              dy);
+      }
     }
     if (lane == 0) {
       L.miscd[0] = e0;

@@ -100,21 +100,24 @@ struct ExactResult {
 //
 // cur/ref: element (0,0) of plane 0 of the block / candidate window, with their
 // own row pitch and plane stride (global planes or staged shared-memory tiles).
+// Partial form: the perfect subtree over chain groups q in [q0, q1) (32 chains,
+// i.e. 4 leaves, per q; q1 - q0 a power of two, q0 a multiple of it), plus the
+// sparsity count of those elements.  Every lane returns the sum (the count is
+// warp-reduced).  q0 = 0, q1 = nq is the whole tree.
 template <typename Elem>
-__device__ ExactResult exact_energy_generic(const Elem* cur, int cpitch, long long cplane, const Elem* ref, int rpitch,
-                                            long long rplane, int b, int P, const double* tab, double tol, double oml,
-                                            double lam) {
+__device__ void exact_partial(const Elem* cur, int cpitch, long long cplane, const Elem* ref, int rpitch,
+                              long long rplane, int b, int P, const double* tab, double tol, int q0, int q1,
+                              double& total_out, int& cnt_out) {
   const int lane = threadIdx.x & 31;
   const int lb = __ffs(b) - 1;
   const int n = P << (2 * lb);
   const int leaf = n < 128 ? n : 128;
   const int rounds = leaf >> 3;
   const int chains = (n / leaf) * 8;
-  const int nq = chains > 32 ? chains / 32 : 1;
   int cnt = 0;
   double stack[16];  // carry depth log2(n/4096): 16 covers any n < 2^28
   double total = 0.0;
-  for (int q = 0; q < nq; ++q) {
+  for (int q = q0; q < q1; ++q) {
     const int c = lane + 32 * q;
     double r = 0.0;
     if (c < chains) {
@@ -137,21 +140,25 @@ __device__ ExactResult exact_energy_generic(const Elem* cur, int cpitch, long lo
     r = __dadd_rn(r, shfl_xor_d(r, 4));
     if (chains > 8) r = __dadd_rn(r, shfl_xor_d(r, 8));
     if (chains > 16) r = __dadd_rn(r, shfl_xor_d(r, 16));
-    if (nq == 1) {
+    if (q1 - q0 == 1) {
       total = r;
     } else {
-      int k = q, lvl = 0;
+      int k = q - q0, lvl = 0;
       while (k & 1) {
         r = __dadd_rn(stack[lvl], r);
         k >>= 1;
         ++lvl;
       }
       stack[lvl] = r;
-      if (q == nq - 1) total = r;
+      if (q == q1 - 1) total = r;
     }
   }
   for (int m = 16; m; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
-  total = __shfl_sync(0xffffffffu, total, 0);  // lanes past `chains` hold partial garbage
+  total_out = __shfl_sync(0xffffffffu, total, 0);  // lanes past `chains` hold partial garbage
+  cnt_out = cnt;
+}
+
+__device__ __forceinline__ ExactResult exact_finish(double total, int cnt, int n, double oml, double lam) {
   const double s_f = __dadd_rn(0.0, total);
   const double nd = (double)n;
   ExactResult res;
@@ -159,6 +166,21 @@ __device__ ExactResult exact_energy_generic(const Elem* cur, int cpitch, long lo
   res.count = cnt;
   res.energy = __dadd_rn(__dmul_rn(oml, __ddiv_rn(s_f, nd)), __dmul_rn(lam, __ddiv_rn((double)cnt, nd)));
   return res;
+}
+
+template <typename Elem>
+__device__ ExactResult exact_energy_generic(const Elem* cur, int cpitch, long long cplane, const Elem* ref, int rpitch,
+                                            long long rplane, int b, int P, const double* tab, double tol, double oml,
+                                            double lam) {
+  const int lb = __ffs(b) - 1;
+  const int n = P << (2 * lb);
+  const int leaf = n < 128 ? n : 128;
+  const int chains = (n / leaf) * 8;
+  const int nq = chains > 32 ? chains / 32 : 1;
+  double total;
+  int cnt;
+  exact_partial<Elem>(cur, cpitch, cplane, ref, rpitch, rplane, b, P, tab, tol, 0, nq, total, cnt);
+  return exact_finish(total, cnt, n, oml, lam);
 }
 
 // Global-memory form: both operands in the same plane layout.
