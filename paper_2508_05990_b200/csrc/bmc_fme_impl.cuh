@@ -1119,6 +1119,53 @@ __device__ StageResult select_block(const SmemLayout& L, const PairCtx<Elem>& pc
     nk = L.misc[5];
     rlist = L.klist2;
   }
+  if (W > 1 && nk < nw) {
+    // fewer replays than warps (large blocks): every replay split across W warps
+    // (aligned subtrees, joined in tree order by thread 0), one after another
+    if (tid == 0) {
+      L.miscd[1] = e0;
+      L.misc[4] = m0;
+    }
+    for (int e = 0; e < nk; ++e) {
+      const int k = rlist[e];
+      if (warp < W) {
+        int dx, dy;
+        const int ki = (int)((k) - fGG.div(k) * g.G), kj = (int)fGG.div(k);
+        cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, ki, kj, dx, dy);
+        double tsum;
+        int tcnt;
+        exact_cand_partial<Elem>(L, pl, g, pc, ox, oy, b, coff_e, ki, kj, dx, dy, warp * (nq / W),
+                                 (warp + 1) * (nq / W), tsum, tcnt);
+        if (lane == 0) {
+          L.best_e[warp] = tsum;
+          L.best_k[warp] = tcnt;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double v[kMaxSW];
+        int cnt = 0;
+        for (int w = 0; w < W; ++w) {
+          v[w] = L.best_e[w];
+          cnt += L.best_k[w];
+        }
+        for (int st = 1; st < W; st *= 2)
+          for (int w = 0; w + st < W; w += 2 * st) v[w] = __dadd_rn(v[w], v[w + st]);
+        const double ek = exact_finish(v[0], cnt, n, pc.oml, pc.lam).energy;
+        if (ek < L.miscd[1] || (ek == L.miscd[1] && k < L.misc[4])) {
+          L.miscd[1] = ek;
+          L.misc[4] = k;
+        }
+      }
+      __syncthreads();
+    }
+    if (nk == 0) __syncthreads();
+    const int kw = L.misc[4];
+    cand_valid_ij(g, ox, oy, b, pc.frame_h, pc.frame_w, (int)((kw) - fGG.div(kw) * g.G), (int)fGG.div(kw), res.dx,
+                  res.dy);
+    res.energy = L.miscd[1];
+    return res;
+  }
   double be = (warp == 0) ? e0 : 1e300;
   int bk = (warp == 0) ? m0 : 0x7fffffff;
   for (int e = warp; e < nk; e += nw) {
