@@ -188,7 +188,7 @@ class ClipSession:
     """
 
     def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
-                 bayer: bool = True, chunks: int = 5, lag: int = 2, weights=None):
+                 bayer: bool = True, chunks: int = 5, lag: int = 2, weights=None, ramp: float = 1.0):
         if config.refine_enabled and config.fme.block_sizes[-1] * (2 if bayer else 1) < CABR_MIN_BLOCK:
             raise ValueError(f"CaBR block size must be at least {CABR_MIN_BLOCK}: the finest FME level yields "
                              f"{config.fme.block_sizes[-1] * (2 if bayer else 1)}-pixel blocks; disable refinement "
@@ -206,7 +206,9 @@ class ClipSession:
         self.copy_out = torch.cuda.Stream()
         t = int(n_frames)
         k = max(1, min(int(chunks), t))
-        bounds = [round(i * t / k) for i in range(k + 1)]
+        # chunk c ends at t * ((c+1)/k)^ramp: ramp > 1 makes the first chunks short, so
+        # the GPU starts after a small H2D while later (longer) copies overlap compute
+        bounds = [round(t * (i / k) ** float(ramp)) for i in range(k + 1)]
         self.chunks = [(bounds[i], bounds[i + 1]) for i in range(k) if bounds[i + 1] > bounds[i]]
         self.lag = max(1, int(lag))
         self.h2d_bytes = 0
