@@ -191,7 +191,7 @@ def _pixels_on_device(frame, torch, dev):
     if isinstance(frame, Frame):
         data = np.ascontiguousarray(frame.data)
         kind = 0 if data.dtype == np.uint8 else 1
-        t = torch.from_numpy(data.view(np.int16) if kind == 1 else data).to(dev)
+        t = torch.from_numpy(np.array(data.view(np.int16) if kind == 1 else data, copy=True)).to(dev)
         return t, kind
     arr = np.ascontiguousarray(np.asarray(frame, dtype=np.float32))
     return torch.from_numpy(arr).to(dev), 2

@@ -437,10 +437,10 @@ __global__ void __launch_bounds__(THREADS, 1) cabr_kernel(const CabrArgs a) {
     conv3x3<16, 1>(sP, rr.p, rc.p, S, 1, sW[0], sW[0] + 144, 16, 2, sE0, rr.e0, rc.e0, false, true);
     ready();
     issue(2);
-    conv3x3<8, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW[1], sW[1] + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
+    conv3x3<16, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW[1], sW[1] + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
     ready();
     issue(3);
-    conv3x3<8, 1>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sE2, rr.e2, rc.e2, false,
+    conv3x3<16, 2>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sE2, rr.e2, rc.e2, false,
                   true);
     __syncthreads();
     // ---- context encoder
@@ -454,21 +454,21 @@ __global__ void __launch_bounds__(THREADS, 1) cabr_kernel(const CabrArgs a) {
     }
     ready();
     issue(4);
-    conv3x3<8, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW[1], sW[1] + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
+    conv3x3<16, 2>(sE0, rr.e0, rc.e0, K + 1, 16, sW[1], sW[1] + 16 * 9 * 32, 32, 2, sE1, rr.e1, rc.e1, false, true);
     ready();
     issue(5);
     const int ne2 = rr.e2.n() * rc.e2.n();
-    conv3x3<8, 1>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sE2 + 32 * ne2, rr.e2, rc.e2,
+    conv3x3<16, 2>(sE1, rr.e1, rc.e1, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sE2 + 32 * ne2, rr.e2, rc.e2,
                   false, true);
     ready();
     issue(6);
     // ---- decoder conv 0 over the 64 fused channels, in two staged halves
     // (image half then context half: one accumulation order, cabr.py:235-237)
     float* sD0 = sE0;  // enc0 maps are dead
-    conv3x3<8, 1>(sE2, rr.e2, rc.e2, K / 2 + 1, 32, sW[1], nullptr, 32, 1, sD0, rr.d0, rc.d0, false, false);
+    conv3x3<16, 2>(sE2, rr.e2, rc.e2, K / 2 + 1, 32, sW[1], nullptr, 32, 1, sD0, rr.d0, rc.d0, false, false);
     ready();
     issue(7);
-    conv3x3<8, 1>(sE2 + 32 * ne2, rr.e2, rc.e2, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sD0, rr.d0, rc.d0,
+    conv3x3<16, 2>(sE2 + 32 * ne2, rr.e2, rc.e2, K / 2 + 1, 32, sW[0], sW[0] + 32 * 9 * 32, 32, 1, sD0, rr.d0, rc.d0,
                   true, true);
     ready();
     if (item + (int)gridDim.x < n_items) issue(0);  // the next item's first layer
