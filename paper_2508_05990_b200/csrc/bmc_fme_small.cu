@@ -48,15 +48,16 @@ __device__ __forceinline__ void word_sc(uint32_t cw, uint32_t rw, uint32_t& S, u
     const uint32_t d2 = mx - mn;
     S = __dp2a_lo(d2, 0x0101u, S);
     const uint32_t f = HIGHD ? (((d2 & 0x7fff7fffu) + k1) & d2) : (((d2 & 0x7fff7fffu) + k1) | d2);
-    C += __popc(f & 0x80008000u);
+    // lane bit 15 set iff d >= D: IDP.2A adds 0x8000 per counted lane (C holds 0x8000 * count)
+    C = __dp2a_lo(f & 0x80008000u, 0x0101u, C);
   }
 }
 
 // (S, C_lo) of one candidate: P planes x b rows of WPR words, reference rows
 // read through L1 with one funnel shift per word (shift 0 for aligned rows).
-// ALIGNED: the row starts on a WPR*4-byte boundary (every candidate of a stage
-// whose step is a multiple of the block row width, e.g. the coarse s = 8 stage
-// of 8x8 blocks): one vector load per row, no shifts.  Plane strides and the
+// ALIGNED: the row starts on an 8-byte boundary with no sub-word shift (the
+// coarse s = 8 and s = 4 stages of 8x8 blocks, half of the unit-step ones):
+// one 16-byte or two 8-byte loads per row, no shifts.  Plane strides and the
 // row pitch are 16-byte multiples, so the alignment holds for every row.
 template <typename Elem, int WPR, bool HIGHD, bool ALIGNED>
 __device__ __forceinline__ void cand_sc(const uint32_t* __restrict__ rrow, long long rpitch_w, long long rplane_w,
@@ -67,8 +68,14 @@ __device__ __forceinline__ void cand_sc(const uint32_t* __restrict__ rrow, long 
     for (int y = 0; y < b; ++y) {
       uint32_t w[WPR + 1];
       if constexpr (ALIGNED && WPR == 4) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(rr));
-        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; w[4] = 0;
+        if (((reinterpret_cast<uintptr_t>(rrow)) & 15) == 0) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(rr));
+          w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        } else {  // 8-byte aligned row
+          const uint2 v0 = __ldg(reinterpret_cast<const uint2*>(rr)), v1 = __ldg(reinterpret_cast<const uint2*>(rr) + 1);
+          w[0] = v0.x; w[1] = v0.y; w[2] = v1.x; w[3] = v1.y;
+        }
+        w[4] = 0;
       } else if constexpr (ALIGNED) {
         const uint2 v = __ldg(reinterpret_cast<const uint2*>(rr));
         w[0] = v.x; w[1] = v.y; w[2] = 0;
@@ -157,7 +164,8 @@ __device__ SmallStage small_stage(const Elem* __restrict__ cur_g, const Elem* __
     uint32_t S = 0, Cacc = 0, a2 = 0;
     const uint32_t* rrow = reinterpret_cast<const uint32_t*>(ref + (long long)(oy + dy) * p.pitch) + xr / EPW;
     const long long rpw = p.pitch / EPW, rplw = p.plane_stride / EPW;
-    const bool al = sh == 0 && (reinterpret_cast<uintptr_t>(rrow) & (wpr * 4 - 1)) == 0;
+    // whole-row vector loads: 16-byte (or, for 4-word rows, 8-byte) aligned rows without a sub-word shift
+    const bool al = sh == 0 && (reinterpret_cast<uintptr_t>(rrow) & 7) == 0;
     if (wpr == 4) {
       if (al) {
         if (highd) cand_sc<Elem, 4, true, true>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
@@ -175,7 +183,7 @@ __device__ SmallStage small_stage(const Elem* __restrict__ cur_g, const Elem* __
         else cand_sc<Elem, 2, false, false>(rrow, rpw, rplw, cur_s, P, b, sh, k1, k2, S, Cacc, a2);
       }
     }
-    int C = EPW == 4 ? ((int)Cacc - (int)a2 + n) / 2 : (int)Cacc;
+    int C = EPW == 4 ? ((int)Cacc - (int)a2 + n) / 2 : (int)(Cacc >> 15);
     if (!count) C = 0;
     const int k = j * G + i;
     const double lb = __dadd_rn(__dmul_rn(p.one_minus_lam, __ddiv_rn((double)S, unit)),
