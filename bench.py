@@ -438,6 +438,9 @@ def run_b200(args, rank, world, local_rank):
                                "(fme_stage_kernel / fme_small_kernel), CUDA events around the ME graph in every "
                                "timed step",
                      "kernel_ms": me_avg, "samples_per_launch": m["samples"],
+                     "achieved_basis": "the reference's full-search samples (sum of candidate_evals x P x b^2, "
+                                       "SURVEY 8d) per second of ME; unit-step stages settle exact-match blocks by "
+                                       "successive elimination (DESIGN 5), so fewer SAD instructions execute",
                      "peak_basis": f"{rate:.0f} samples/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz (measured SAD issue "
                                    "rate, tools/sad_peak.cu)",
                      "hbm": {"algorithmic_bytes": me_bytes, "achieved_gbs": me_bytes / (me_avg / 1e3) / 1e9,
