@@ -454,8 +454,138 @@ __global__ void __launch_bounds__(kDecideThreads) decide_max_kernel(const Decide
   }
 }
 
+// ---------------------------------------------------------------------------
+// AEM scan for large accumulator grids ("max" statistic): the serial
+// dependence of the scan is only through the per-frame maximum, and the
+// accumulator of every cell after frame t is a function of the last reset
+// point alone -- acc_t(r) = (((base + p_{r+1}) + p_{r+2}) + ... + p_t) with
+// base = 0 after a key frame r, or the carried-in accumulator when no key
+// happened in this call (the reference's own float64 order, frame_select.py:99).
+// So the maxima M(r, t) of every possible reset point r are computed in
+// parallel (aem_prefix_max_kernel: one CTA per (cell chunk, r, stream), a CTA
+// max per frame, one atomicMax per CTA on the ordered bits of non-negative
+// doubles), a single thread per stream then walks the frames with
+// trigger_t = M(last reset, t) (aem_scan_kernel), and the final accumulator is
+// rebuilt from the last reset point (aem_final_acc_kernel).  Identical
+// decisions, triggers and state to the per-frame scan.
+// ---------------------------------------------------------------------------
+constexpr int kAemThreads = 1024;
+constexpr int kAemCellsPerThread = 4;
+
+__global__ void __launch_bounds__(kAemThreads) aem_prefix_max_kernel(const DecideArgs a, unsigned long long* M) {
+  __shared__ double red[kAemThreads / 32];
+  const int stream = blockIdx.z, ri = blockIdx.y;  // ri = 0: carried-in accumulator; ri >= 1: key at t_begin+ri-1
+  const bmc_select_params& sp = a.sp;
+  const int ncoarse = sp.coarse_h * sp.coarse_w;
+  const int nt = a.t_end - a.t_begin;
+  const int t0 = ri == 0 ? a.t_begin : a.t_begin + ri;  // first frame accumulated from this reset point
+  const double* accg = a.acc + (long long)stream * ncoarse;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cbase = blockIdx.x * kAemThreads * kAemCellsPerThread + threadIdx.x;
+  double acc[kAemCellsPerThread];
+#pragma unroll
+  for (int k = 0; k < kAemCellsPerThread; ++k) {
+    const int c = cbase + k * kAemThreads;
+    acc[k] = (ri == 0 && c < ncoarse) ? accg[c] : 0.0;
+  }
+  unsigned long long* Mrow = M + ((long long)stream * nt + ri) * nt;
+  for (int t = t0; t < a.t_end; ++t) {
+    const double* e = a.energy + stream * a.ess + t * a.efs;
+    double mx = 0.0;  // accumulators are sums of non-negative energies
+#pragma unroll
+    for (int k = 0; k < kAemCellsPerThread; ++k) {
+      const int c = cbase + k * kAemThreads;
+      if (c < ncoarse) {
+        acc[k] = __dadd_rn(acc[k], pooled_cell(e, c, sp));
+        mx = fmax(mx, acc[k]);
+      }
+    }
+    for (int m = 16; m; m >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (warp == 0) {
+      double r = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+      for (int m = 16; m; m >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, m));
+      if (lane == 0) atomicMax(Mrow + (t - a.t_begin), (unsigned long long)__double_as_longlong(r));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void aem_scan_kernel(const DecideArgs a, const unsigned long long* M, int32_t* reset_out) {
+  const int stream = blockIdx.x * blockDim.x + threadIdx.x;
+  if (stream >= a.n_streams) return;
+  const bmc_select_params& sp = a.sp;
+  const int nt = a.t_end - a.t_begin;
+  const unsigned long long* Ms = M + (long long)stream * nt * nt;
+  int fsk = a.fsk[stream], last_key = a.last_key[stream];
+  int ri = 0;  // current reset point (row of M)
+  for (int t = a.t_begin; t < a.t_end; ++t) {
+    const double r = __longlong_as_double((long long)Ms[(long long)ri * nt + (t - a.t_begin)]);
+    const int f = fsk + 1;
+    const bool key = r > sp.aem_threshold || (sp.has_max_gop && f >= sp.max_gop);
+    int kind, ref;
+    if (key) {
+      kind = 0;
+      ref = -1;
+      fsk = 0;
+      last_key = t;
+      ri = t - a.t_begin + 1;
+    } else if (sp.policy_keyframe) {
+      kind = 2;
+      ref = last_key;
+      fsk = f;
+    } else {
+      kind = 1;
+      ref = t - 1;
+      fsk = f;
+    }
+    const long long o = (long long)stream * a.dss + t;
+    a.kind[o] = kind;
+    a.ref[o] = ref;
+    a.trigger[o] = r;
+    if (a.ref_next) a.ref_next[stream] = stream * a.frames_per_stream + (sp.policy_keyframe ? last_key : t);
+  }
+  a.fsk[stream] = fsk;
+  a.last_key[stream] = last_key;
+  reset_out[stream] = ri;
+}
+
+__global__ void aem_final_acc_kernel(const DecideArgs a, const int32_t* reset) {
+  const int stream = blockIdx.y;
+  const bmc_select_params& sp = a.sp;
+  const int ncoarse = sp.coarse_h * sp.coarse_w;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncoarse) return;
+  const int ri = reset[stream];
+  double* accg = a.acc + (long long)stream * ncoarse;
+  double v = ri == 0 ? accg[c] : 0.0;
+  for (int t = ri == 0 ? a.t_begin : a.t_begin + ri; t < a.t_end; ++t)
+    v = __dadd_rn(v, pooled_cell(a.energy + stream * a.ess + t * a.efs, c, sp));
+  accg[c] = v;
+}
+
 int launch_decide(const DecideArgs& a, cudaStream_t st) {
   const int ncoarse = a.sp.coarse_h * a.sp.coarse_w;
+  const int nt = a.t_end - a.t_begin;
+  if (!a.sp.statistic_mean && ncoarse > kDecideThreads * kDecideCells && nt >= 1) {
+    // stream-ordered scratch (capturable): M (streams, nt, nt) + the final reset point per stream
+    const size_t mbytes = (size_t)a.n_streams * nt * nt * sizeof(unsigned long long);
+    void* ws = nullptr;
+    int rc = cuda_status(cudaMallocAsync(&ws, mbytes + (size_t)a.n_streams * sizeof(int32_t), st), "AEM scratch");
+    if (rc) return rc;
+    unsigned long long* M = static_cast<unsigned long long*>(ws);
+    int32_t* reset = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + mbytes);
+    if ((rc = cuda_status(cudaMemsetAsync(M, 0, mbytes, st), "AEM scratch"))) return rc;
+    const int chunks = (ncoarse + kAemThreads * kAemCellsPerThread - 1) / (kAemThreads * kAemCellsPerThread);
+    aem_prefix_max_kernel<<<dim3(chunks, nt, a.n_streams), kAemThreads, 0, st>>>(a, M);
+    if ((rc = cuda_status(cudaGetLastError(), "aem_prefix_max_kernel"))) return rc;
+    aem_scan_kernel<<<(a.n_streams + 63) / 64, 64, 0, st>>>(a, M, reset);
+    if ((rc = cuda_status(cudaGetLastError(), "aem_scan_kernel"))) return rc;
+    aem_final_acc_kernel<<<dim3((ncoarse + 255) / 256, a.n_streams), 256, 0, st>>>(a, reset);
+    if ((rc = cuda_status(cudaGetLastError(), "aem_final_acc_kernel"))) return rc;
+    return cuda_status(cudaFreeAsync(ws, st), "AEM scratch");
+  }
   if (!a.sp.statistic_mean && ncoarse <= kDecideThreads * kDecideCells) {
     decide_max_kernel<<<a.n_streams, kDecideThreads, 0, st>>>(a);
     return cuda_status(cudaGetLastError(), "decide_max_kernel");

@@ -515,3 +515,56 @@ def test_search_stage_any_block_size(cuda, bsize):
             assert got[0] == tuple(mv) and np.float64(got[1]).view(np.int64) == np.float64(e).view(np.int64)
     with pytest.raises(ValueError, match="all candidate windows fall outside"):
         fme.search_stage(a / 1.0, b / 1.0, (0, 0), bsize, (-30, -30), 1, 1, cfg)
+
+
+@pytest.mark.parametrize("max_gop", [None, 4])
+@pytest.mark.parametrize("policy", ["previous", "keyframe"])
+def test_decide_large_grid_parallel_scan(cuda, max_gop, policy):
+    """AEM scans over accumulator grids too large for the register-resident kernel take the
+    parallel form (maxima of every reset point, then a serial scan): per-frame calls and one
+    call over a frame range, split in two resumable calls, all equal the oracle bit for bit."""
+    import ctypes
+    from paper_2508_05990_b200 import _native as N, fme, frame_select as fs
+    rng = np.random.default_rng(23)
+    for (ch, cw, f) in [(90, 120, 1), (60, 70, 2)]:
+        T = 14
+        es = [rng.random((ch * f, cw * f)) * 0.03 for _ in range(T)]
+        # oracle
+        acc, fsk, last_key = np.zeros((ch, cw)), 0, 0
+        want = []
+        for i in range(1, T):
+            kind, ref, trig, acc, fsk = O.decide(acc, fsk, 32, es[i], 32 // f, i, 0.15, max_gop, "max", policy, last_key)
+            want.append((kind, ref, trig))
+            if kind == "key":
+                last_key = i
+        # per-frame drop-in calls
+        st = fs.AemState.fresh(cw, ch, 32)
+        lk = 0
+        for i in range(1, T):
+            field = fme.MotionField(32 // f, cw * f, ch * f, np.zeros((ch * f, cw * f, 2), np.int64), es[i],
+                                    np.ones_like(es[i], bool))
+            d, st = fs.decide(st, field, i, 0.15, max_gop, "max", policy, lk)
+            assert (d.kind.value, d.reference_index, d.trigger_statistic) == want[i - 1]
+            if d.kind.value == "key":
+                lk = i
+        np.testing.assert_array_equal(st.accumulated, acc)
+        # frame-range calls straight through the C ABI, split at frame 6
+        dev = cuda.device("cuda")
+        e = cuda.from_numpy(np.stack(es)).to(dev)
+        sp = N.select_params(ch * f, cw * f, f, ch, cw, "max", policy, max_gop, 0.15)
+        accd = cuda.zeros((ch, cw), dtype=cuda.float64, device=dev)
+        fskd = cuda.zeros(1, dtype=cuda.int32, device=dev)
+        lkd = cuda.zeros(1, dtype=cuda.int32, device=dev)
+        kind = cuda.zeros(T, dtype=cuda.int32, device=dev)
+        ref = cuda.full((T,), -1, dtype=cuda.int32, device=dev)
+        trig = cuda.zeros(T, dtype=cuda.float64, device=dev)
+        cells = ch * f * cw * f
+        for t0, t1 in ((1, 6), (6, T)):
+            N.check(N.load().bmc_decide(N.ptr(e), cells, cells, 1, t0, t1, ctypes.byref(sp), N.ptr(accd), N.ptr(fskd),
+                                        N.ptr(lkd), N.ptr(kind), N.ptr(ref), N.ptr(trig), T, None, T,
+                                        N.stream_handle()))
+        k, r, tr = kind.cpu().numpy(), ref.cpu().numpy(), trig.cpu().numpy()
+        names = ["key", "nonkey_prev_ref", "nonkey_key_ref"]
+        for i in range(1, T):
+            assert (names[k[i]], None if r[i] < 0 else int(r[i]), float(tr[i])) == want[i - 1]
+        np.testing.assert_array_equal(accd.cpu().numpy(), acc)
