@@ -125,13 +125,27 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+            # the sampler is live (first row written) before the timed region starts
+            deadline = time.time() + 5.0
+            while time.time() < deadline and not self._rows():
+                time.sleep(0.05)
+            self._n0 = len(self._rows())
         except Exception:
             self.proc = None
         return self
 
+    def _rows(self):
+        try:
+            return [r for r in self.path.read_text().strip().splitlines() if r.count(",") >= 7]
+        except OSError:
+            return []
+
     def __exit__(self, *exc):
         if self.proc is not None:
+            # short timed regions (< the 100 ms period): wait for the sample that covers their end
+            deadline = time.time() + 1.0
+            while time.time() < deadline and len(self._rows()) <= self._n0:
+                time.sleep(0.02)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)

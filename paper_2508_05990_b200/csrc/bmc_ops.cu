@@ -569,7 +569,25 @@ int launch_decide(const DecideArgs& a, cudaStream_t st) {
   const int ncoarse = a.sp.coarse_h * a.sp.coarse_w;
   const int nt = a.t_end - a.t_begin;
   if (!a.sp.statistic_mean && ncoarse > kDecideThreads * kDecideCells && nt >= 1) {
-    // stream-ordered scratch (capturable): M (streams, nt, nt) + the final reset point per stream
+    // stream-ordered scratch (capturable): M (streams, nt, nt) + the final reset point per stream.
+    // The device's default pool keeps its memory mapped between uses (release
+    // threshold raised once per device): otherwise every synchronize trims it and
+    // the next allocation pays for mapping pages again.
+    {
+      static std::mutex mu;
+      static bool done[64] = {false};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> g(mu);
+      if (dev >= 0 && dev < 64 && !done[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          unsigned long long thr = ~0ull;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done[dev] = true;
+      }
+    }
     const size_t mbytes = (size_t)a.n_streams * nt * nt * sizeof(unsigned long long);
     void* ws = nullptr;
     int rc = cuda_status(cudaMallocAsync(&ws, mbytes + (size_t)a.n_streams * sizeof(int32_t), st), "AEM scratch");
