@@ -341,12 +341,25 @@ def measure(name, args, rank, world, local_rank, stream_ids, flush):
     keyframes = int((kinds == 0).sum())
 
     # --- e2e through the public host-buffer API, every stream of this rank ---
-    sess = ClipSession(pcfg, H, W, T, dt, True, weights=weights)
     host_in = [(torch.from_numpy(cl).pin_memory(),
                 torch.from_numpy(np.stack([labs[t].classes for t in range(T)])).pin_memory()) for cl, labs in clips]
-    for _ in range(2):
+    # one session, clips in turn (ClipPool overlaps two sessions but must copy predicted labels out
+    # of the session buffers: 12.7k vs 14.1k frames/s on C4, see DESIGN)
+    sess = ClipSession(pcfg, H, W, T, dt, True, weights=weights)
+    totals = {"h2d": 0, "d2h": 0}
+
+    def run_all():
+        totals["h2d"] = totals["d2h"] = 0
+        res = []
         for raw_k, key_k in host_in:
-            sess.run(raw_k, key_k)
+            res.append(sess.run(raw_k, key_k))
+            totals["h2d"] += sess.h2d_bytes
+            totals["d2h"] += sess.d2h_bytes
+        return res
+
+    counts = lambda: (totals["h2d"], totals["d2h"])  # noqa: E731
+    for _ in range(2):
+        run_all()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -355,13 +368,10 @@ def measure(name, args, rank, world, local_rank, stream_ids, flush):
         flush_l2()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h2d = d2h = 0
-        for raw_k, key_k in host_in:
-            out_labels, _k, _r, _t = sess.run(raw_k, key_k)
-            h2d += sess.h2d_bytes
-            d2h += sess.d2h_bytes
+        outs = run_all()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    e2e_ok = bool(np.array_equal(np.stack(out_labels), eng.labels[S - 1].cpu().numpy()))
+        h2d, d2h = counts()
+    e2e_ok = bool(np.array_equal(np.stack(outs[-1][0]), eng.labels[S - 1].cpu().numpy()))
     flagged = 0
     if weights is not None:
         mt = eng.levels[-1].matched[:eng.n_pairs].cpu().numpy()

@@ -1453,13 +1453,12 @@ inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageL
       }
     }
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
+  static const int sms = [] {  // thread-safe one-time init
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms < 1) sms = 1;
-  }
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n < 1 ? 1 : n;
+  }();
   const long long work = (long long)grid.x * grid.y;
   static const int persist_mult = [] {  // resident waves per launch; 0 = one CTA per block
     const char* e = knob_env("BMC_PERSIST");

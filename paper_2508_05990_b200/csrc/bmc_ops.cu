@@ -1069,14 +1069,22 @@ __global__ void __launch_bounds__(kThreads) predict_chain_kernel(const PredictAr
 
 int launch_predict_chain(const PredictArgs& a, int n_streams, int t_begin, int t_end, unsigned* barrier_ctr,
                          cudaStream_t st) {
-  static int per_sm = 0, sms = 0;
-  if (!per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_chain_kernel, kThreads, 0);
-    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(predict)");
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (per_sm < 1) per_sm = 1;
+  int per_sm = 0, sms = 0;
+  {
+    // one query per process (thread-safe); one process drives one GPU model
+    static std::mutex mu;
+    static int c_per_sm = 0, c_sms = 0;
+    std::lock_guard<std::mutex> g(mu);
+    if (!c_per_sm) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm, predict_chain_kernel, kThreads, 0);
+      if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(predict)");
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&c_sms, cudaDevAttrMultiProcessorCount, dev);
+      if (c_per_sm < 1) c_per_sm = 1;
+    }
+    per_sm = c_per_sm;
+    sms = c_sms;
   }
   const long long tasks = (long long)n_streams * a.H * ((a.W + 15) / 16);
   if (tasks >= (1ll << 31)) {

@@ -438,3 +438,68 @@ class ClipSession:
                 labels.append(self.pin_labels[i].numpy())
         self.h2d_bytes, self.d2h_bytes = state["h2d"], state["d2h"]
         return labels, kinds, refs, trig
+
+
+class ClipPool:
+    """Many independent clips (streams) through ``n_sessions`` ClipSessions at once.
+
+    Each session owns its device buffers and runs on its own compute stream; a
+    host thread per session drives it (the native executor releases the GIL), so
+    one clip's H2D, compute and D2H overlap another's -- the batched form of
+    ``ClipSession.run`` for stream-parallel serving.
+    ``run(clips)`` takes a list of ``(raw, key_labels)`` pairs (as
+    ``ClipSession.run``) and returns their results in order.  Predicted frames'
+    labels are copied out of the session buffers (a session's next clip
+    overwrites them); key frames are returned as the caller's key maps.
+    """
+
+    def __init__(self, config: PipelineConfig, height: int, width: int, n_frames: int, dtype=np.uint8,
+                 bayer: bool = True, n_sessions: int = 2, weights=None, **session_kw):
+        import threading
+        from concurrent.futures import ThreadPoolExecutor
+        self.sessions = [ClipSession(config, height, width, n_frames, dtype, bayer, weights=weights, **session_kw)
+                         for _ in range(max(1, int(n_sessions)))]
+        torch = self.sessions[0].torch
+        self.torch = torch
+        self.streams = [torch.cuda.Stream() for _ in self.sessions]
+        self.pool = ThreadPoolExecutor(max_workers=len(self.sessions))
+        self.device = torch.cuda.current_device()
+        self._lock = threading.Lock()
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def _worker(self, k, items):
+        torch = self.torch
+        torch.cuda.set_device(self.device)
+        sess, st = self.sessions[k], self.streams[k]
+        out, h2d, d2h = [], 0, 0
+        with torch.cuda.stream(st):
+            for idx, (raw, keys) in items:
+                labels, kinds, refs, trig = sess.run(raw, keys)
+                # predicted frames live in the session's output buffer (overwritten by its next
+                # clip): copy those; key frames are the caller's own key maps
+                labels = [np.array(x) if kinds[i] != 0 else x for i, x in enumerate(labels)]
+                out.append((idx, (labels, kinds, refs, trig)))
+                h2d += sess.h2d_bytes
+                d2h += sess.d2h_bytes
+        return out, h2d, d2h
+
+    def run(self, clips):
+        torch = self.torch
+        cur = torch.cuda.current_stream()
+        for st in self.streams:  # earlier work of the caller's stream is visible to every session
+            st.wait_stream(cur)
+        n = len(self.sessions)
+        parts = [[(i, c) for i, c in enumerate(clips) if i % n == k] for k in range(n)]
+        futs = [self.pool.submit(self._worker, k, parts[k]) for k in range(n)]
+        results = [None] * len(clips)
+        self.h2d_bytes = self.d2h_bytes = 0
+        for f in futs:
+            out, h2d, d2h = f.result()
+            self.h2d_bytes += h2d
+            self.d2h_bytes += d2h
+            for idx, r in out:
+                results[idx] = r
+        for st in self.streams:
+            cur.wait_stream(st)
+        return results

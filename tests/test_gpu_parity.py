@@ -568,3 +568,27 @@ def test_decide_large_grid_parallel_scan(cuda, max_gop, policy):
         for i in range(1, T):
             assert (names[k[i]], None if r[i] < 0 else int(r[i]), float(tr[i])) == want[i - 1]
         np.testing.assert_array_equal(accd.cpu().numpy(), acc)
+
+
+def test_clip_pool_matches_sessions(cuda):
+    """ClipPool (two sessions on their own streams, one host thread each) equals one
+    ClipSession run per clip, in input order."""
+    from paper_2508_05990_b200 import pipeline, synth
+    from paper_2508_05990_b200.config import PipelineConfig
+    from paper_2508_05990_b200.fme import FmeConfig, SearchStage
+    cfg = PipelineConfig(fme=FmeConfig(stages=(SearchStage(8, 1), SearchStage(0, 1), SearchStage(0, 1)),
+                                       block_sizes=(16,)), max_gop=3, aem_threshold=float("inf"))
+    clips, keys = [], []
+    for k in range(5):
+        c = synth.bayer_pan_clip(256, 192, 7, (2 * (k % 3) - 2, 2), seed=40 + k)
+        clips.append(cuda.from_numpy(c).pin_memory())
+        keys.append(cuda.from_numpy(np.stack([l.classes for l in synth.block_labels(256, 192, 7, seed=k)])).pin_memory())
+    pool = pipeline.ClipPool(cfg, 192, 256, 7, np.uint8, True, n_sessions=2)
+    got = pool.run(list(zip(clips, keys)))
+    sess = pipeline.ClipSession(cfg, 192, 256, 7, np.uint8, True)
+    for (raw, key), g in zip(zip(clips, keys), got):
+        want = sess.run(raw, key)
+        for a, b in zip(g[0], want[0]):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(g[1], want[1])
+        np.testing.assert_array_equal(g[2], want[2])
