@@ -85,7 +85,8 @@ int bmc_confusion(const uint8_t* pred, const uint8_t* truth, int64_t n, int n_ma
  * weight_spec(num_classes) (cabr.py:97-119) in order, float32, concatenated
  * (exactly the bytes after the JSON header of save_weights, cabr.py:152-168),
  * already in device memory; bmc_cabr_pack_weights re-lays it out for the
- * kernel into `packed` (bmc_cabr_weight_floats(num_classes) floats).
+ * kernel into `packed` (bmc_cabr_weight_floats(num_classes) floats: the
+ * payload re-laid out plus the decoder's merged row taps).
  * num_classes <= 256 (uint8 labels); block sizes K >= 16, multiples of 16.
  *
  * bmc_cabr_forward_blocks: cabr_forward(extract_patch(frame, labels, origin, K))

@@ -172,10 +172,11 @@ def packed_weights(weights: CabrWeights, torch, dev):
     if key not in per:
         C = weights.num_classes
         src = torch.from_numpy(weights.payload()).to(dev)
-        n = N.load().bmc_cabr_weight_floats(C)
-        if src.numel() != n:
-            raise ValueError(f"weight payload holds {src.numel()} floats, the network needs {n}")
-        dst = torch.empty(n, dtype=torch.float32, device=dev)
+        need = sum(int(np.prod(shape)) for _, shape in weight_spec(C))
+        if src.numel() != need:
+            raise ValueError(f"weight payload holds {src.numel()} floats, the network needs {need}")
+        # the packed layout adds the decoder's merged row taps (bmc_cabr_weight_floats)
+        dst = torch.empty(N.load().bmc_cabr_weight_floats(C), dtype=torch.float32, device=dev)
         N.check(N.load().bmc_cabr_pack_weights(N.ptr(src), C, N.ptr(dst), N.stream_handle()))
         per[key] = dst
     return per[key]
@@ -369,7 +370,8 @@ def executed_flops(block_size: int, num_classes: int) -> int:
             total += 2 * (2 * 9 * 16 * 32 * a["e1"])          # img/ctx enc.1
             total += 2 * (2 * 9 * 32 * 32 * a["e2"])          # img/ctx enc.2
             total += 2 * 9 * 64 * 32 * a["d0"]                # dec.0
-            total += 2 * 9 * 32 * 32 * ts * ts + 2 * 32 * c * ts * ts  # dec.1 + head
+            # dec.1: rows u % 4 in {1, 2} read one dec.0 row (3 merged taps), the others 9 taps
+            total += 2 * 6 * 32 * 32 * ts * ts + 2 * 32 * c * ts * ts  # dec.1 + head
     return total
 
 

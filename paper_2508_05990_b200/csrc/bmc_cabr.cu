@@ -69,6 +69,25 @@ __host__ __device__ inline WOff cabr_offsets(int C) {
   return o;
 }
 
+// dec.1 over the x4 nearest-upsampled map: output rows u with u % 4 in {1, 2}
+// read the same dec.0 row for all three kernel rows, so their three row taps
+// collapse into one (W[ky=0] + W[ky=1]) + W[ky=2] -- stored (c, kx, o) after
+// the payload, 16-byte aligned.  Rows with u % 4 in {0, 3} straddle two dec.0
+// rows and keep the 3x3 weights.
+constexpr int kMergedFloats = 32 * 3 * 32;
+__host__ __device__ inline long long cabr_merged_offset(const WOff& o) { return (o.total + 3) & ~3ll; }
+__host__ __device__ inline long long cabr_packed_floats(const WOff& o) { return cabr_merged_offset(o) + kMergedFloats; }
+
+__global__ void cabr_merge_rows_kernel(float* __restrict__ packed, WOff o) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (c, kx, oc)
+  if (i >= kMergedFloats) return;
+  const int oc = i % 32, kx = (i / 32) % 3, c = i / 96;
+  const float* w = packed + o.w[7];  // dec.1 weights, (cin, tap, cout)
+  const float v = __fadd_rn(__fadd_rn(w[(c * 9 + kx) * 32 + oc], w[(c * 9 + 3 + kx) * 32 + oc]),
+                            w[(c * 9 + 6 + kx) * 32 + oc]);
+  packed[cabr_merged_offset(o) + i] = v;
+}
+
 __global__ void cabr_pack_kernel(const float* __restrict__ src, float* __restrict__ dst, WOff o) {
   const long long n = o.total;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -119,7 +138,7 @@ struct CabrGeo {
   int K, ts, tiles, threads;
   int np, ne0, ne1, ne2, nd0;  // max region sides over the tile positions
   int off_p, off_e0, off_e1, off_e2, off_w, off_lab;  // float offsets (off_lab: byte offset)
-  int wfloats;
+  int wfloats, wfloats1;
   int smem;
 };
 
@@ -279,90 +298,100 @@ __device__ void ctx_conv0_onehot(const uint8_t* __restrict__ lab, Range rp, Rang
 template <int PX>
 __device__ void dec1_head(const float* __restrict__ d0, Range rd, Range cd, int l0r, int l0c, int ts,
                           const float* __restrict__ w1, const float* __restrict__ b1, const float* __restrict__ hw,
-                          const float* __restrict__ hb, int C, const CabrArgs& a, int item, int bx, int by, int ty0,
-                          int tx0, int stream) {
+                          const float* __restrict__ hb, const float* __restrict__ wm, int C, const CabrArgs& a,
+                          int item, int bx, int by, int ty0, int tx0, int stream) {
   const int K = a.g.K;
   const int wD = cd.n(), plane = rd.n() * wD;
-  const int npix = ts * ts;
-  const int half = threadIdx.x & 1;
-  const int ngrp = npix / PX;  // ts is a multiple of PX: a group is PX pixels of one row
-  // every warp runs the same number of iterations (the head's shuffles need all lanes)
-  for (int base = 0; base < ngrp; base += blockDim.x >> 1) {
-    const int pg = base + (threadIdx.x >> 1);
-    const bool ok = pg < ngrp;
-    const int i = ok ? (pg * PX) / ts : 0, j0 = ok ? (pg * PX) % ts : 0;
-    const int u = l0r + i;
-    int roff[3], coff[PX][3];
+  const int half = threadIdx.x & 1, warp = threadIdx.x >> 5;
+  // Pixels are assigned by row class u % 4 (u = l0r + i, the row in the x4 grid)
+  // so every warp takes one class: classes 1 and 2 read one dec.0 row (merged
+  // weights, 3 taps), classes 0 and 3 two (3x3 weights).  A warp's 16 lane pairs
+  // cover 16 groups of PX pixels of one row; ts/4 rows per class.
+  const int gpr = ts / PX;                          // groups per row
+  const int wpc = (int)(blockDim.x >> 5) / 4;       // warps per class
+  const int cls = warp / wpc;
+  const int g = (warp - cls * wpc) * 16 + (threadIdx.x & 31) / 2;
+  const int i = ((cls - l0r) & 3) + 4 * (g / gpr), j0 = (g % gpr) * PX;
+  const int u = l0r + i;
+  const bool merged = cls == 1 || cls == 2;
+  int roff[3], coff[PX][3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) roff[k] = (((u - 1 + k) >> 2) - rd.lo) * wD;
+  for (int k = 0; k < 3; ++k) roff[k] = (((u - 1 + k) >> 2) - rd.lo) * wD;
 #pragma unroll
-    for (int p = 0; p < PX; ++p)
+  for (int p = 0; p < PX; ++p)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) coff[p][k] = ((l0c + j0 + p - 1 + k) >> 2) - cd.lo;
-    float acc[PX][16];
+    for (int k = 0; k < 3; ++k) coff[p][k] = ((l0c + j0 + p - 1 + k) >> 2) - cd.lo;
+  float acc[PX][16];
 #pragma unroll
-    for (int p = 0; p < PX; ++p)
+  for (int p = 0; p < PX; ++p)
 #pragma unroll
-      for (int o = 0; o < 16; ++o) acc[p][o] = 0.f;
+    for (int o = 0; o < 16; ++o) acc[p][o] = 0.f;
+  auto step = [&](const float* ip, const float* wrow, int r) {
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      float x[PX];
+#pragma unroll
+      for (int p = 0; p < PX; ++p) x[p] = ip[r + coff[p][kx]];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 wv = *reinterpret_cast<const float4*>(wrow + kx * 32 + 4 * j);
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          acc[p][4 * j + 0] = fmaf(x[p], wv.x, acc[p][4 * j + 0]);
+          acc[p][4 * j + 1] = fmaf(x[p], wv.y, acc[p][4 * j + 1]);
+          acc[p][4 * j + 2] = fmaf(x[p], wv.z, acc[p][4 * j + 2]);
+          acc[p][4 * j + 3] = fmaf(x[p], wv.w, acc[p][4 * j + 3]);
+        }
+      }
+    }
+  };
+  if (merged) {
+    for (int c = 0; c < 32; ++c) step(d0 + c * plane, wm + c * 96 + 16 * half, roff[1]);
+  } else {
     for (int c = 0; c < 32; ++c) {
       const float* ip = d0 + c * plane;
       const float* wp = w1 + c * 9 * 32 + 16 * half;
 #pragma unroll
-      for (int tap = 0; tap < 9; ++tap) {
-        float x[PX];
-#pragma unroll
-        for (int p = 0; p < PX; ++p) x[p] = ip[roff[tap / 3] + coff[p][tap % 3]];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 wv = *reinterpret_cast<const float4*>(wp + tap * 32 + 4 * j);
-#pragma unroll
-          for (int p = 0; p < PX; ++p) {
-            acc[p][4 * j + 0] = fmaf(x[p], wv.x, acc[p][4 * j + 0]);
-            acc[p][4 * j + 1] = fmaf(x[p], wv.y, acc[p][4 * j + 1]);
-            acc[p][4 * j + 2] = fmaf(x[p], wv.z, acc[p][4 * j + 2]);
-            acc[p][4 * j + 3] = fmaf(x[p], wv.w, acc[p][4 * j + 3]);
-          }
-        }
-      }
+      for (int ky = 0; ky < 3; ++ky) step(ip, wp + ky * 96, roff[ky]);
     }
+  }
 #pragma unroll
-    for (int p = 0; p < PX; ++p)
+  for (int p = 0; p < PX; ++p)
 #pragma unroll
-      for (int o = 0; o < 16; ++o) acc[p][o] = fmaxf(acc[p][o] + b1[16 * half + o], 0.f);
-    float best[PX];
-    int arg[PX];
-    for (int o = 0; o < C; ++o) {
-      const float* hr = hw + o * 32 + 16 * half;
-      float l[PX];
-#pragma unroll
-      for (int p = 0; p < PX; ++p) {
-        float v = 0.f;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v = fmaf(acc[p][c], hr[c], v);
-        l[p] = v;
-      }
-#pragma unroll
-      for (int p = 0; p < PX; ++p) {
-        // (low half + high half) in the same order on both lanes
-        const float other = __shfl_xor_sync(0xffffffffu, l[p], 1);
-        const float lo = half ? other : l[p], hi = half ? l[p] : other;
-        const float v = (lo + hi) + hb[o];
-        if (o == 0 || v > best[p]) {
-          best[p] = v;
-          arg[p] = o;
-        }
-        if (a.logits && half == 0 && ok) a.logits[(((long long)item * C + o) * K + ty0 + i) * K + tx0 + j0 + p] = v;
-      }
-    }
-    if (half || !ok) continue;
+    for (int o = 0; o < 16; ++o) acc[p][o] = fmaxf(acc[p][o] + b1[16 * half + o], 0.f);
+  float best[PX];
+  int arg[PX];
+  for (int o = 0; o < C; ++o) {
+    const float* hr = hw + o * 32 + 16 * half;
+    float l[PX];
 #pragma unroll
     for (int p = 0; p < PX; ++p) {
-      const int yb = ty0 + i, xb = tx0 + j0 + p;  // position inside the K x K block
-      if (a.argmax) a.argmax[((long long)item * K + yb) * K + xb] = (uint8_t)arg[p];
-      if (a.scratch) {
-        const int fy = by + yb, fx = bx + xb;
-        if (fy < a.H && fx < a.W) a.scratch[stream * a.scr_ss + (long long)fy * a.W + fx] = (uint8_t)arg[p];
+      float v = 0.f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v = fmaf(acc[p][c], hr[c], v);
+      l[p] = v;
+    }
+#pragma unroll
+    for (int p = 0; p < PX; ++p) {
+      // (low half + high half) in the same order on both lanes
+      const float other = __shfl_xor_sync(0xffffffffu, l[p], 1);
+      const float lo = half ? other : l[p], hi = half ? l[p] : other;
+      const float v = (lo + hi) + hb[o];
+      if (o == 0 || v > best[p]) {
+        best[p] = v;
+        arg[p] = o;
       }
+      if (a.logits && half == 0) a.logits[(((long long)item * C + o) * K + ty0 + i) * K + tx0 + j0 + p] = v;
+    }
+  }
+  if (half) return;
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    const int yb = ty0 + i, xb = tx0 + j0 + p;  // position inside the K x K block
+    if (a.argmax) a.argmax[((long long)item * K + yb) * K + xb] = (uint8_t)arg[p];
+    if (a.scratch) {
+      const int fy = by + yb, fx = bx + xb;
+      if (fy < a.H && fx < a.W) a.scratch[stream * a.scr_ss + (long long)fy * a.W + fx] = (uint8_t)arg[p];
     }
   }
 }
@@ -379,15 +408,16 @@ __global__ void __launch_bounds__(THREADS, 1) cabr_kernel(const CabrArgs a) {
   float* sE0 = smem + g.off_e0;
   float* sE1 = smem + g.off_e1;
   float* sE2 = smem + g.off_e2;
-  float* sW[2] = {smem + g.off_w, smem + g.off_w + g.wfloats};
+  float* sW[2] = {smem + g.off_w, smem + g.off_w + g.wfloats};  // buffer 1 holds wfloats1 (dec.1 + head + merged)
   uint8_t* sLab = reinterpret_cast<uint8_t*>(smem) + g.off_lab;
   constexpr int PXD = 2 * TS * TS / THREADS;  // decoder pixels per lane pair
   // The item's eight weight stages, double-buffered: stage j lands in sW[j & 1]
   // while the layer before it computes from the other buffer.
   const float* wsrc[8] = {a.wts + wo.w[0], a.wts + wo.w[1], a.wts + wo.w[2], a.wts + wo.w[4],
                           a.wts + wo.w[5], a.wts + wo.w[6], a.wts + wo.w[6] + 32 * 9 * 32, a.wts + wo.w[7]};
+  const int moff = (int)(cabr_merged_offset(wo) - wo.w[7]);  // merged dec.1 rows, relative to stage 7
   const int wlen[8] = {9 * 16 + 16, 16 * 9 * 32 + 32, 32 * 9 * 32 + 32, 16 * 9 * 32 + 32, 32 * 9 * 32 + 32,
-                       32 * 9 * 32, 32 * 9 * 32 + 32, 32 * 9 * 32 + 32 + C * 32 + C};
+                       32 * 9 * 32, 32 * 9 * 32 + 32, moff + kMergedFloats};
   auto issue = [&](int j) { stage_weights_async(sW[j & 1], wsrc[j], wlen[j]); };
   auto ready = [&]() {
     cp_async_wait_all();
@@ -475,7 +505,7 @@ __global__ void __launch_bounds__(THREADS, 1) cabr_kernel(const CabrArgs a) {
     // ---- decoder conv 1 + head + argmax
     float* w7 = sW[1];
     dec1_head<PXD>(sD0, rr.d0, rc.d0, rr.l0, rc.l0, TS, w7, w7 + 32 * 9 * 32, w7 + 32 * 9 * 32 + 32,
-                   w7 + 32 * 9 * 32 + 32 + C * 32, C, a, e, bx, by, ty0, tx0, stream);
+                   w7 + 32 * 9 * 32 + 32 + C * 32, w7 + moff, C, a, e, bx, by, ty0, tx0, stream);
     __syncthreads();
   }
 }
@@ -507,13 +537,15 @@ int plan_cabr(CabrGeo& g, int K, int C) {
   const int fe0 = up4(std::max(16 * g.ne0 * g.ne0, 32 * g.nd0 * g.nd0));  // dec0 output reuses enc0
   const int fe1 = up4(32 * g.ne1 * g.ne1);
   const int fe2 = up4(64 * g.ne2 * g.ne2);
-  g.wfloats = up4(std::max(32 * 9 * 32 + 32, 32 * 9 * 32 + 32 + C * 32 + C));
+  const WOff wo = cabr_offsets(C);
+  g.wfloats = up4(32 * 9 * 32 + 32);  // buffer 0: the even stages
+  g.wfloats1 = up4((int)(cabr_packed_floats(wo) - wo.w[7]));  // buffer 1 also takes stage 7 (dec.1 + head + merged)
   g.off_p = 0;
   g.off_e0 = g.off_p + fp;
   g.off_e1 = g.off_e0 + fe0;
   g.off_e2 = g.off_e1 + fe1;
   g.off_w = g.off_e2 + fe2;  // two weight buffers (double-buffered stages)
-  g.off_lab = 4 * (g.off_w + 2 * g.wfloats);
+  g.off_lab = 4 * (g.off_w + g.wfloats + g.wfloats1);
   g.smem = g.off_lab + ((g.np * g.np + 15) & ~15);
   if (g.smem > 227 * 1024) {
     set_error("CaBR tile needs %d bytes of shared memory", g.smem);
@@ -705,7 +737,7 @@ using namespace bmc;
 
 extern "C" size_t bmc_cabr_weight_floats(int num_classes) {
   if (num_classes < 1) return 0;
-  return (size_t)cabr_offsets(num_classes).total;
+  return (size_t)cabr_packed_floats(cabr_offsets(num_classes));
 }
 
 extern "C" int bmc_cabr_pack_weights(const float* payload, int num_classes, float* packed, void* stream) {
@@ -714,7 +746,9 @@ extern "C" int bmc_cabr_pack_weights(const float* payload, int num_classes, floa
     return BMC_E_ARG;
   }
   const WOff o = cabr_offsets(num_classes);
-  cabr_pack_kernel<<<64, 256, 0, static_cast<cudaStream_t>(stream)>>>(payload, packed, o);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cabr_pack_kernel<<<64, 256, 0, st>>>(payload, packed, o);
+  cabr_merge_rows_kernel<<<(kMergedFloats + 255) / 256, 256, 0, st>>>(packed, o);
   return cuda_status(cudaGetLastError(), "cabr_pack_kernel");
 }
 
