@@ -616,18 +616,22 @@ template <typename Elem>
 __device__ uint32_t warp_sad(const SmemLayout& L, const StagePlan& pl, int P, int b, int cur_w0, int xo, int yo) {
   constexpr int EPW = 4 / sizeof(Elem);
   const int lane = threadIdx.x & 31;
-  const int lwpr = __ffs(b / EPW) - 1, lb = __ffs(b) - 1;  // b and b/EPW are powers of two
-  const int total = P << (lb + lwpr);
+  const int wpr = b / EPW;                     // words per block row (2..16, a power of two)
+  const int rows_per_iter = 32 / wpr;          // block rows one warp step covers
+  const int wc = lane & (wpr - 1), r0 = lane / wpr;
   const int bww = pl.bw / EPW, cbw = pl.cbw / EPW;
-  const int sh = (xo % EPW) * 8 * (int)sizeof(Elem), w0 = xo / EPW;
+  const int sh = (xo % EPW) * 8 * (int)sizeof(Elem);
   uint32_t acc = 0;
-  for (int idx = lane; idx < total; idx += 32) {
-    const int w = idx & ((1 << lwpr) - 1), py = idx >> lwpr;  // py = p * b + y
-    const int p = py >> lb, y = py & (b - 1);
-    const uint32_t* rr = L.win + (p * pl.wrows + yo + y) * bww + w0 + w;
-    const uint32_t lo = rr[0];
-    const uint32_t rw = sh ? __funnelshift_r(lo, rr[1], sh) : lo;
-    acc = sad_word(L.cur[py * cbw + cur_w0 + w], rw, acc, Elem());
+  for (int p = 0; p < P; ++p) {
+    // fixed word column per lane, pointers advanced by whole row groups
+    const uint32_t* rr = L.win + (p * pl.wrows + yo + r0) * bww + xo / EPW + wc;
+    const uint32_t* cr = L.cur + (p * b + r0) * cbw + cur_w0 + wc;
+    for (int y = r0; y < b; y += rows_per_iter) {
+      const uint32_t lo = rr[0];
+      acc = sad_word(cr[0], sh ? __funnelshift_r(lo, rr[1], sh) : lo, acc, Elem());
+      rr += rows_per_iter * bww;
+      cr += rows_per_iter * cbw;
+    }
   }
   for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
   return acc;
