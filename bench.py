@@ -50,6 +50,10 @@ CONFIGS = {
     "c2gop": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
               "C2 clip with a fixed key interval (max_gop=6, aem=inf): 25 predicted frames, ring-vote refinement",
               {"max_gop": 6, "aem_threshold": float("inf"), "refine_enabled": True}),
+    # C2 with +-2 levels of seeded sensor noise per frame: no block has an exact (zero-SAD)
+    # match, so successive elimination never settles a block and the dense screening runs
+    "c2noise": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint8",
+                "C2 clip with +-2 levels of per-frame sensor noise (no exact matches)", {}),
     "c2u16": (1920, 1080, 30, (4, -2), 5, ((16, 1), (0, 1), (0, 1)), (16,), "uint16",
               "1920x1080 RGGB uint16 30-frame pan clip (C2's uint16 variant), 16x16 blocks, +-16 full search", {}),
     "c1": (256, 256, 8, (2, 2), 3, ((8, 1), (0, 1), (0, 1)), (16,), "uint8",
@@ -102,6 +106,9 @@ def make_clip(name, seed_offset=0):
         if v is None:  # c4: per-stream velocity
             v = c4_velocity(seed_offset)
         clip = synth.bayer_pan_clip(w, h, t, v, seed=seed + seed_offset, dtype=dt)
+    if name == "c2noise":
+        rng = np.random.default_rng(77 + seed_offset)
+        clip = np.clip(clip.astype(np.int16) + rng.integers(-2, 3, clip.shape, dtype=np.int16), 0, 255).astype(dt)
     labels = synth.block_labels(w, h, t, seed=seed + seed_offset)
     return clip, labels
 
