@@ -616,22 +616,18 @@ template <typename Elem>
 __device__ uint32_t warp_sad(const SmemLayout& L, const StagePlan& pl, int P, int b, int cur_w0, int xo, int yo) {
   constexpr int EPW = 4 / sizeof(Elem);
   const int lane = threadIdx.x & 31;
-  const int wpr = b / EPW;                     // words per block row (2..16, a power of two)
-  const int rows_per_iter = 32 / wpr;          // block rows one warp step covers
-  const int wc = lane & (wpr - 1), r0 = lane / wpr;
+  const int lwpr = __ffs(b / EPW) - 1, lb = __ffs(b) - 1;  // b and b/EPW are powers of two
+  const int total = P << (lb + lwpr);
   const int bww = pl.bw / EPW, cbw = pl.cbw / EPW;
-  const int sh = (xo % EPW) * 8 * (int)sizeof(Elem);
+  const int sh = (xo % EPW) * 8 * (int)sizeof(Elem), w0 = xo / EPW;
   uint32_t acc = 0;
-  for (int p = 0; p < P; ++p) {
-    // fixed word column per lane, pointers advanced by whole row groups
-    const uint32_t* rr = L.win + (p * pl.wrows + yo + r0) * bww + xo / EPW + wc;
-    const uint32_t* cr = L.cur + (p * b + r0) * cbw + cur_w0 + wc;
-    for (int y = r0; y < b; y += rows_per_iter) {
-      const uint32_t lo = rr[0];
-      acc = sad_word(cr[0], sh ? __funnelshift_r(lo, rr[1], sh) : lo, acc, Elem());
-      rr += rows_per_iter * bww;
-      cr += rows_per_iter * cbw;
-    }
+  for (int idx = lane; idx < total; idx += 32) {
+    const int w = idx & ((1 << lwpr) - 1), py = idx >> lwpr;  // py = p * b + y
+    const int p = py >> lb, y = py & (b - 1);
+    const uint32_t* rr = L.win + (p * pl.wrows + yo + y) * bww + w0 + w;
+    const uint32_t lo = rr[0];
+    const uint32_t rw = sh ? __funnelshift_r(lo, rr[1], sh) : lo;
+    acc = sad_word(L.cur[py * cbw + cur_w0 + w], rw, acc, Elem());
   }
   for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
   return acc;
@@ -768,10 +764,6 @@ __device__ bool sea_screen(const SmemLayout& L, const StageGeom& g, int b, const
   }
   if (tid == 0) L.misc[9] = 0;
   __syncthreads();
-  // an exact match has bound 0: a block whose smallest bound is positive has none,
-  // and only exact-match blocks are settled here
-  for (int kb = 0; kb < nblk; ++kb)
-    if (L.seaM[kb] > 0) return false;
   // Two rounds of exact SADs: (1) every candidate at the smallest bound -- the
   // exact match, where the content has one, has bound 0 -- giving T = their
   // smallest SAD; (2) every remaining candidate with bound <= T.  Only rows
@@ -873,12 +865,6 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
   if (!SHIFT && pl.copies)
     for (int i = 0; i < min(g.G, EPW); ++i) phase_mask |= 1u << ((g.d + i * s) % EPW);
 
-  // SEA attempt / fallback counters of the launch, loaded early (used after the barrier)
-  unsigned sea_att = 0, sea_fb = 0;
-  if (tid == 0 && pl.sea && pl.sea_stats) {
-    sea_att = *((volatile unsigned*)pl.sea_stats);
-    sea_fb = *((volatile unsigned*)pl.sea_stats + 1);
-  }
   __syncthreads();  // previous users of smem are done; mbarrier init visible
   if (tid == 0) L.misc[10] = 0;  // set to 1 below when the SEA screening settles the stage
   if (pl.use_tma && pl.pg == pc.P && !(phase_mask & ~1u) && !pl.debug) {
@@ -889,12 +875,6 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
       mbar_expect_tx(L.bar, (uint32_t)(pl.tma_bytes));  // full boxes, OOB included
       tma_load_3d(L.win, tm_win, g.tx0, g.wy0, pc.ref_z, L.bar);
       tma_load_3d(L.cur, tm_cur, cx0, oy, pc.cur_z, L.bar);
-      if (pl.sea) {
-        // Adaptive SEA: once 64 CTAs of the launch have tried and most fell back
-        // (content without exact matches, e.g. sensor noise), the remaining CTAs go
-        // straight to the dense screening.  The counters steer cost, never results.
-        L.misc[11] = !(sea_att >= 64 && 2 * sea_fb > sea_att);
-      }
     }
     if (pl.split && !pl.sea)
       for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
@@ -902,23 +882,14 @@ __device__ StageGeom stage_sad(const SmemLayout& L, const PairCtx<Elem>& pc, con
     mbar_wait(L.bar, phase);
     phase ^= 1;
     if (pl.sea) {
-      if (L.misc[11]) {  // set by thread 0 before the barrier above
-        const bool done = pc.P == 4 ? sea_screen<Elem, 4>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h)
-                                    : sea_screen<Elem, 1>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h);
-        if (tid == 0 && pl.sea_stats) {
-          atomicAdd(pl.sea_stats, 1u);
-          if (!done) atomicAdd(pl.sea_stats + 1, 1u);
-        }
-        if (done) {
-          if (tid == 0) L.misc[10] = 1;
-          __syncthreads();
-          return g;
-        }
-        if (pl.split) {  // dense fallback: its split tail items accumulate with atomics
-          for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
-          __syncthreads();
-        }
-      } else if (pl.split) {
+      const bool done = pc.P == 4 ? sea_screen<Elem, 4>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h)
+                                  : sea_screen<Elem, 1>(L, g, b, pl, coff_w, nblk, ox, oy, pc.frame_w, pc.frame_h);
+      if (done) {
+        if (tid == 0) L.misc[10] = 1;
+        __syncthreads();
+        return g;
+      }
+      if (pl.split) {  // dense fallback: its split tail items accumulate with atomics
         for (int k = tid; k < nblk * pl.parts * g.G * g.G; k += blockDim.x) L.sad[k] = 0;
         __syncthreads();
       }
@@ -1441,30 +1412,11 @@ inline bool sync_debug() {
   return v == 1;
 }
 
-inline unsigned* sea_stats_buffer() {
-  // one (attempts, fallbacks) pair per device; concurrent launches on other streams
-  // share it, which only blurs the heuristic
-  static std::mutex mu;
-  static unsigned* bufs[64] = {nullptr};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> g(mu);
-  if (!bufs[dev] && cudaMalloc(&bufs[dev], 2 * sizeof(unsigned)) != cudaSuccess) bufs[dev] = nullptr;
-  return bufs[dev];
-}
-
 template <typename E, int CW, int TY, bool SH>
 inline int launch_one(const CUtensorMap& tw, const CUtensorMap& tc, const StageLaunch& a, dim3 grid, cudaStream_t st) {
   int rc = set_smem(fme_stage_kernel<E, CW, TY, SH>, a.plan.smem);
   if (rc) return rc;
   StageLaunch la = a;
-  if (la.plan.sea) {
-    la.plan.sea_stats = sea_stats_buffer();
-    if (la.plan.sea_stats &&
-        (rc = cuda_status(cudaMemsetAsync(la.plan.sea_stats, 0, 2 * sizeof(unsigned), st), "SEA stats reset")))
-      return rc;
-  }
   la.gwg = (uint32_t)((a.gw + a.kblk - 1) / a.kblk);
   la.total = a.single ? 1u : la.gwg * (uint32_t)a.gh * (uint32_t)a.n_pairs;
   static const bool plan_log = [] {

@@ -34,7 +34,6 @@ struct StagePlan {
   int off_vc;     // byte offset of the SEA column-sum region ([P][G][bw] uint16 (u8) / uint32 (u16))
   int sea_cap;    // max survivors per CTA before falling back to dense screening
   int vcs;        // SEA column-sum row stride (elements; an odd number of 32-bit words: no bank conflicts)
-  unsigned* sea_stats;  // SEA attempts / fallbacks of the launch (device; set by the launcher, may be NULL)
 };
 
 #ifndef BMC_STAGE_THREADS
